@@ -1,0 +1,68 @@
+"""Exception types raised by the B200 dichotomy path.
+
+The names, base class and ``SingularPivot.row`` attribute follow the
+reference hierarchy (``pkg/src/blocktri/errors.py:4-33``) so code written
+against ``blocktri`` catches the same failures.  When the reference package
+is importable, :mod:`paper_1108_4181_b200.install` swaps these for the
+reference classes themselves so ``except blocktri.errors.X`` keeps working.
+"""
+
+
+class BlocktriError(Exception):
+    """Root of every error this package raises (ref errors.py:4)."""
+
+
+class DimensionMismatch(BlocktriError):
+    """Block counts / block orders of the operands disagree (ref errors.py:8)."""
+
+
+class SingularBlock(BlocktriError):
+    """A dense block is singular to working precision (ref errors.py:12)."""
+
+
+class SingularPivot(BlocktriError):
+    """Singular pivot block inside a sweep; ``row`` is the block row local to
+    the factored (sub)matrix, exactly as the reference reports it
+    (ref errors.py:16-21, _kernels.pyx:159-160)."""
+
+    def __init__(self, row, message=None):
+        self.row = row
+        super().__init__(message or f"singular pivot block at block row {row}")
+
+
+class IndexOutOfRange(BlocktriError):
+    """Block-row index outside the valid range (ref errors.py:28)."""
+
+
+class InvalidRankCount(BlocktriError):
+    """ranks < 1 or ranks > N (ref errors.py:32, dichotomy.py:326-327)."""
+
+
+class InconsistentRanges(BlocktriError):
+    """Ranges do not tile the matrix (ref errors.py:36)."""
+
+
+class DeviceError(BlocktriError):
+    """CUDA / NCCL failure or missing native library (no reference analogue:
+    the reference never leaves the host)."""
+
+
+_BY_NAME = {
+    c.__name__: c
+    for c in (BlocktriError, DimensionMismatch, SingularBlock, SingularPivot,
+              IndexOutOfRange, InvalidRankCount, InconsistentRanges, DeviceError)
+}
+
+
+def rebind(module) -> None:
+    """Use another module's same-named exception classes (e.g. blocktri.errors)."""
+    g = globals()
+    for name in list(_BY_NAME):
+        cls = getattr(module, name, None)
+        if isinstance(cls, type) and issubclass(cls, Exception):
+            g[name] = cls
+            _BY_NAME[name] = cls
+
+
+def get(name):
+    return _BY_NAME[name]
