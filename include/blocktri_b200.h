@@ -1,0 +1,97 @@
+/*
+ * blocktri_b200.h -- C ABI of the B200-native many-RHS block-tridiagonal
+ * dichotomy solver (arXiv 1108.4181, Algorithm 2).
+ *
+ * This is the drop-in boundary for the reference path
+ *   blocktri.dichotomy.plan_build(p_matrix, ranks) -> DichotomyPlan
+ *       (/root/reference/pkg/src/blocktri/dichotomy.py:318-338)
+ *   blocktri.dichotomy.plan_solve(plan, f_batch)   -> X
+ *       (/root/reference/pkg/src/blocktri/dichotomy.py:358-390)
+ * The reference has no FFI of its own (pure Python + a Cython kernel module,
+ * _kernels.pyx:111-194); these entry points are what its dichotomy module
+ * binds through ctypes.  Plain pointers and sizes only.
+ *
+ * Storage convention (ref core.py:1-10, 84-90): row i of the operator reads
+ *   -lower[i-1] x_{i-1} + diag[i] x_i - upper[i] x_{i+1} = f_i
+ * diag is (n,m,m), lower/upper are (n-1,m,m), all row-major float64;
+ * right-hand sides / solutions are (n,m,k) row-major float64.
+ */
+#ifndef BLOCKTRI_B200_H
+#define BLOCKTRI_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The Python host maps them to the reference exception
+ * classes (ref errors.py): 1 -> DimensionMismatch, 2 -> SingularPivot(row),
+ * 3 -> InvalidRankCount; the rest -> DeviceError. */
+enum {
+  BTD_OK = 0,
+  BTD_ERR_DIMENSION = 1,
+  BTD_ERR_SINGULAR_PIVOT = 2,
+  BTD_ERR_INVALID_RANKS = 3,
+  BTD_ERR_CUDA = 4,
+  BTD_ERR_NCCL = 5,
+  BTD_ERR_OOM = 6,
+  BTD_ERR_INVALID_ARG = 7,
+  BTD_ERR_UNSUPPORTED = 8
+};
+
+/* flags for btd_plan_create */
+enum {
+  BTD_MATRIX_ON_DEVICE = 1 /* diag/lower/upper are device pointers on `device` */
+};
+
+typedef struct btd_plan btd_plan;
+
+typedef struct btd_plan_info {
+  int64_t n, m, mp;          /* block rows, block order, padded order (multiple of 8) */
+  int64_t ranks;             /* reference P (ranges of the Algorithm-2 partition) */
+  int64_t split;             /* device sub-ranges per reference range (1 = exact ref. partition) */
+  int64_t nranges;           /* device ranges actually used (= ranks*split clamped to n) */
+  int64_t L;                 /* uniform range length; the last range may be shorter */
+  int64_t tree_nodes, tree_depth;
+  int64_t factor_bytes;      /* HBM held by the plan */
+  int64_t row_lo, row_hi;    /* block rows owned by this plan (sharded plans) */
+  int32_t device;
+  int32_t mode;              /* 0 = fused chain kernels, 1 = per-step GEMM sweep (large m) */
+} btd_plan_info;
+
+/* Algorithm 2 step 1 (ref dichotomy.py:318-338): validate 1 <= ranks <= n
+ * (BTD_ERR_INVALID_RANKS), partition rows into ranges K_q = q*L with
+ * L = ceil(n / (ranks*split)), factor every range's interior sweep, assemble
+ * the reduced interface system (Eq. 7) and the inverse rows of its partition
+ * tree.  On BTD_ERR_SINGULAR_PIVOT *err_row holds the row local to the
+ * factored submatrix, exactly as the reference's SingularPivot.row.
+ * `stream` is a cudaStream_t (NULL = legacy default stream). */
+int btd_plan_create(const double* diag, const double* lower, const double* upper,
+                    int64_t n, int64_t m, int64_t ranks, int64_t split,
+                    int device, int flags, void* stream,
+                    btd_plan** out_plan, int64_t* err_row);
+
+/* Algorithm 2 step 2 (ref dichotomy.py:358-390) on DEVICE buffers:
+ * f, x are (n,m,k) float64 on the plan's device; x may alias f.
+ * Stream-ordered; returns once enqueued.  No block factorization. */
+int btd_plan_solve(btd_plan* plan, const double* f, double* x, int64_t k, void* stream);
+
+/* Same on HOST buffers (the reference's numpy-in / numpy-out contract): copies
+ * f to the device, solves, copies x back, synchronizes `stream`. */
+int btd_plan_solve_host(btd_plan* plan, const double* f_host, double* x_host, int64_t k,
+                        void* stream);
+
+int btd_plan_destroy(btd_plan* plan);
+int btd_plan_query(const btd_plan* plan, btd_plan_info* info);
+
+/* Kernel launches issued by this library since load (the bench's
+ * gpu_launches evidence) and the last error text. */
+int64_t btd_launch_count(void);
+const char* btd_last_error(void);
+int btd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLOCKTRI_B200_H */

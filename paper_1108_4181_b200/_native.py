@@ -1,0 +1,102 @@
+"""ctypes binding of the C ABI in include/blocktri_b200.h.
+
+The shared library is built in-tree (``python -m paper_1108_4181_b200.build``
+or ``__graft_entry__.build()``) into ``paper_1108_4181_b200/_lib``.  There is
+no fallback: a missing library or a machine without a CUDA device raises
+:class:`~paper_1108_4181_b200.errors.DeviceError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import errors as _err
+
+LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
+LIB_PATH = os.path.join(LIB_DIR, "libblocktri_b200.so")
+
+BTD_OK = 0
+BTD_ERR_DIMENSION = 1
+BTD_ERR_SINGULAR_PIVOT = 2
+BTD_ERR_INVALID_RANKS = 3
+BTD_MATRIX_ON_DEVICE = 1
+
+# Every symbol include/blocktri_b200.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "btd_plan_create",
+    "btd_plan_solve",
+    "btd_plan_solve_host",
+    "btd_plan_destroy",
+    "btd_plan_query",
+    "btd_launch_count",
+    "btd_last_error",
+    "btd_version",
+)
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64), ("m", ctypes.c_int64), ("mp", ctypes.c_int64),
+        ("ranks", ctypes.c_int64), ("split", ctypes.c_int64), ("nranges", ctypes.c_int64),
+        ("L", ctypes.c_int64), ("tree_nodes", ctypes.c_int64), ("tree_depth", ctypes.c_int64),
+        ("factor_bytes", ctypes.c_int64), ("row_lo", ctypes.c_int64), ("row_hi", ctypes.c_int64),
+        ("device", ctypes.c_int32), ("mode", ctypes.c_int32),
+    ]
+
+
+_lib = None
+
+
+def load():
+    """Load the library once; raise DeviceError (never fall back) if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise _err.DeviceError(
+            f"native library missing: {LIB_PATH} (run `python -m paper_1108_4181_b200.build`)")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32, dp = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+    lib.btd_plan_create.argtypes = [dp, dp, dp, i64, i64, i64, i64, i32, i32, vp,
+                                    ctypes.POINTER(vp), ctypes.POINTER(i64)]
+    lib.btd_plan_create.restype = i32
+    lib.btd_plan_solve.argtypes = [vp, dp, dp, i64, vp]
+    lib.btd_plan_solve.restype = i32
+    lib.btd_plan_solve_host.argtypes = [vp, dp, dp, i64, vp]
+    lib.btd_plan_solve_host.restype = i32
+    lib.btd_plan_destroy.argtypes = [vp]
+    lib.btd_plan_destroy.restype = i32
+    lib.btd_plan_query.argtypes = [vp, ctypes.POINTER(PlanInfo)]
+    lib.btd_plan_query.restype = i32
+    lib.btd_launch_count.argtypes = []
+    lib.btd_launch_count.restype = i64
+    lib.btd_last_error.argtypes = []
+    lib.btd_last_error.restype = ctypes.c_char_p
+    lib.btd_version.argtypes = []
+    lib.btd_version.restype = i32
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    msg = load().btd_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(status: int, err_row: int = -1) -> None:
+    """Map a C status to the reference exception classes (ref errors.py)."""
+    if status == BTD_OK:
+        return
+    msg = last_error()
+    if status == BTD_ERR_DIMENSION:
+        raise _err.DimensionMismatch(msg)
+    if status == BTD_ERR_SINGULAR_PIVOT:
+        raise _err.SingularPivot(int(err_row), msg)
+    if status == BTD_ERR_INVALID_RANKS:
+        raise _err.InvalidRankCount(msg)
+    raise _err.DeviceError(f"status {status}: {msg}")
+
+
+def launch_count() -> int:
+    return int(load().btd_launch_count())

@@ -1,0 +1,980 @@
+// Plan construction, solve orchestration and the C ABI (include/blocktri_b200.h).
+//
+// Algorithm 2 of arXiv 1108.4181 as implemented by the reference
+// (/root/reference/pkg/src/blocktri/dichotomy.py), re-laid out for B200:
+//
+//  plan (once per matrix; ref dichotomy.py:318-338)
+//    * the matrix is identity-padded to npad = P*L rows exactly as the
+//      reference does (ref dichotomy.py:307-315, 328-330), so the device plan
+//      has the reference's ranges, reduced system and partition tree;
+//    * per range, a batched (over ranges) sweep over the L-1 interior rows:
+//        D_j = C_g - A_g S_{j-1}           GEMM   (ref _kernels.pyx:163-168)
+//        Dinv_j = D_j^{-1}                 Gauss-Jordan, reference pivot test
+//        S_j = Dinv_j B_g, AD_j = Dinv_j A_g,
+//        G_j = AD_j G_{j-1}  (left-boundary response, ref U of dichotomy.py:186-188)
+//        Tb_j = B_lo S_0..S_{j-1}          (first-row transfer, gives B_lo W[1])
+//      all in HBM: 5 blocks of mp x mp per interior row;
+//    * reduced three-point system (ref dichotomy.py:212-236) from BU = B_lo U[1],
+//      BV = B_lo V[1], G/S of the last interior row;
+//    * inverse rows of every partition-tree node by transposed block sweeps
+//      with unit right-hand sides (ref dichotomy.py:134-146, 298-304), then the
+//      end corrections E = R[:, :M] A~, H = R[:, -M:] B~ of Algorithm 1.
+//  solve (per K right-hand sides; ref dichotomy.py:358-390)
+//    forward chain kernel -> interface RHS GEMM -> tree: z = R f~ (all nodes,
+//    one launch) then one launch per tree level x~_k = z + E x~_{lo-1} +
+//    H x~_{hi+1} -> backward chain kernel.  Block orders above 256 run the
+//    sweeps as one batched GEMM launch per row step instead (mode 1).
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "blocktri_b200.h"
+#include "btd_chain.cuh"
+#include "btd_gemm.cuh"
+#include "btd_inv.cuh"
+
+using namespace btd;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+struct BtdError {
+  int code;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) {
+  g_err = msg;
+  throw BtdError{code};
+}
+
+void ck(cudaError_t e, const char* what, int line) {
+  if (e != cudaSuccess) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "CUDA error %s (%s) at btd_api.cu:%d: %s", cudaGetErrorName(e),
+             cudaGetErrorString(e), line, what);
+    cudaGetLastError();
+    fail(e == cudaErrorMemoryAllocation ? BTD_ERR_OOM : BTD_ERR_CUDA, buf);
+  }
+}
+#define CK(x) ck((x), #x, __LINE__)
+#define CK_LAUNCH()                                   \
+  do {                                                \
+    g_launches.fetch_add(1, std::memory_order_relaxed); \
+    ck(cudaGetLastError(), "kernel launch", __LINE__); \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void alloc(size_t b) {
+    release();
+    if (b == 0) b = 16;
+    CK(cudaMalloc(&p, b));
+    bytes = b;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  double* d() const { return static_cast<double*>(p); }
+  int64_t* i64() const { return static_cast<int64_t*>(p); }
+  int32_t* i32() const { return static_cast<int32_t*>(p); }
+};
+
+__global__ void pad_blocks_kernel(const double* src, int64_t nsrc, int m, double* dst, int64_t ndst,
+                                  int mp, int diag_identity) {
+  const int64_t total = ndst * mp * mp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / ((int64_t)mp * mp);
+    const int r = (int)((e / mp) % mp), c = (int)(e % mp);
+    double v;
+    if (b < nsrc && r < m && c < m)
+      v = src[(b * m + r) * m + c];
+    else
+      v = (diag_identity && r == c && (b >= nsrc || r >= m)) ? 1.0 : 0.0;
+    dst[e] = v;
+  }
+}
+
+__global__ void set_identity_kernel(double* dst, int mp) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < mp * mp; e += gridDim.x * blockDim.x)
+    dst[e] = (e / mp == e % mp) ? 1.0 : 0.0;
+}
+
+// R_node[a][i*mp + c] = Y_i[c][a]  (ref dichotomy.py:145: y.transpose(2,0,1))
+__global__ void assemble_rows_kernel(const double* Y, const int64_t* ynb0, const int64_t* roff,
+                                     const int64_t* size, const int64_t* eoff, int nnodes,
+                                     int64_t total, int mp, double* R) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = nnodes - 1;  // node with eoff[b] <= e < eoff[b+1]
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (eoff[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    const int b = lo;
+    const int64_t le = e - eoff[b];
+    const int64_t s = size[b];
+    const int64_t a = le / (s * mp), rest = le % (s * mp);
+    const int64_t i = rest / mp, c = rest % mp;
+    R[roff[b] + a * s * mp + i * mp + c] = Y[(ynb0[b] + i) * (int64_t)mp * mp + c * mp + a];
+  }
+}
+
+Opnd mk(const double* base, const int64_t* idx, int64_t add, int64_t stride, int64_t ld,
+        const int64_t* ld_arr = nullptr) {
+  Opnd o;
+  o.base = base;
+  o.idx = idx;
+  o.add = add;
+  o.stride = stride;
+  o.ld = ld;
+  o.ld_arr = ld_arr;
+  return o;
+}
+Opnd none() { return mk(nullptr, nullptr, 0, 0, 0); }
+Term term(Opnd A, Opnd B, int64_t k, double alpha = 1.0, const int64_t* k_arr = nullptr) {
+  Term t;
+  t.A = A;
+  t.B = B;
+  t.k = k;
+  t.k_arr = k_arr;
+  t.alpha = alpha;
+  return t;
+}
+
+void launch_gemm(int64_t rows, int64_t cols, int nbatch, Opnd C, Opnd Cin, double beta,
+                 std::initializer_list<Term> terms, cudaStream_t st) {
+  if (nbatch <= 0 || rows <= 0 || cols <= 0) return;
+  GemmDesc d;
+  memset(&d, 0, sizeof d);
+  d.rows = rows;
+  d.cols = cols;
+  d.nbatch = nbatch;
+  d.C = C;
+  d.Cin = Cin;
+  d.beta = beta;
+  d.nterms = 0;
+  for (const Term& t : terms) d.t[d.nterms++] = t;
+  const int gz = std::min(nbatch, 65535);
+  if (rows <= 32 || cols <= 32) {
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32), gz);
+    gemm_batched_kernel<32, 32><<<grid, 128, 0, st>>>(d);
+  } else {
+    dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64), gz);
+    gemm_batched_kernel<64, 64><<<grid, 128, 0, st>>>(d);
+  }
+  CK_LAUNCH();
+}
+
+struct Node {
+  int64_t lo, hi, k, level;
+};
+
+std::vector<Node> partition_tree(int64_t count, int64_t* depth) {
+  // BFS, split k = lo + (hi-lo+1)//2  (ref dichotomy.py:28-57)
+  std::vector<Node> out;
+  std::vector<std::pair<int64_t, int64_t>> frontier{{0, count - 1}}, nxt;
+  int64_t level = 0;
+  while (!frontier.empty()) {
+    nxt.clear();
+    for (auto& f : frontier) {
+      int64_t lo = f.first, hi = f.second, k = lo + (hi - lo + 1) / 2;
+      out.push_back({lo, hi, k, level});
+      if (k - 1 >= lo) nxt.push_back({lo, k - 1});
+      if (k + 1 <= hi) nxt.push_back({k + 1, hi});
+    }
+    frontier.swap(nxt);
+    ++level;
+  }
+  int64_t d = 0;
+  while ((int64_t(1) << d) < count) ++d;
+  *depth = d;
+  return out;
+}
+
+}  // namespace
+
+struct btd_plan {
+  int device = 0;
+  int64_t n = 0, m = 0, mp = 0, ranks = 0, split = 1, nr = 0, L = 0, npad = 0, cap = 0;
+  int mode = 0;
+  int64_t blk = 0;
+  std::vector<int64_t> lo, slot0;
+  std::vector<int32_t> nint;  // interior rows inside [0, n)
+  std::vector<std::unique_ptr<DevBuf>> arrays;
+  const int64_t* d_lo = nullptr;
+  const int64_t* d_slot0 = nullptr;
+  const int32_t* d_nint = nullptr;
+  DevBuf pool;
+  int64_t off_AD = 0, off_Dinv = 0, off_S = 0, off_G = 0, off_Tb = 0, off_Fc = 0, off_Bif = 0,
+          off_BU = 0, off_BV = 0, off_Dt = 0, off_Rd = 0, off_Rl = 0, off_Ru = 0, off_RdT = 0,
+          off_RlT = 0, off_RuT = 0, off_Z = 0, off_I = 0;
+  // tree
+  std::vector<Node> nodes;
+  int64_t depth = 0;
+  DevBuf Rrows, EH;
+  const int64_t *d_roff = nullptr, *d_rld = nullptr, *d_nlo = nullptr;
+  struct Level {
+    int count = 0;
+    const int64_t *c_idx = nullptr, *z_idx = nullptr, *e_idx = nullptr, *xl_idx = nullptr,
+                  *h_idx = nullptr, *xh_idx = nullptr;
+  };
+  std::vector<Level> levels;
+  // interface-RHS carry batch
+  int ncarry = 0;
+  const int64_t *carry_q = nullptr, *carry_fc = nullptr, *carry_row = nullptr;
+  // mode-1 per-step batches
+  struct Step1 {
+    int cnt = 0;          // ranges active at this step (prefix)
+    int nx = 0, nt = 0;   // bwd: entries whose next row is interior / is x~_{q+1}
+    const int64_t *x_row = nullptr, *x_slot = nullptr, *x_q = nullptr;
+    const int64_t *t_row = nullptr, *t_slot = nullptr, *t_q = nullptr;
+  };
+  std::vector<Step1> steps1;
+  const int64_t* d_qiota = nullptr;
+  int nlive = 0;  // ranges whose interface row is < n
+  // scratch
+  int64_t scratch_k = 0;
+  DevBuf base, zbuf, xt, hostio;
+  int64_t hostio_k = 0;
+  std::mutex mu;
+  cudaStream_t last_stream = nullptr;
+  int64_t factor_bytes = 0;
+
+  template <class T>
+  const T* upload(const std::vector<T>& v) {
+    auto b = std::make_unique<DevBuf>();
+    b->alloc(std::max<size_t>(v.size() * sizeof(T), 16));
+    if (!v.empty()) CK(cudaMemcpy(b->p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    const T* p = static_cast<const T*>(b->p);
+    arrays.push_back(std::move(b));
+    return p;
+  }
+  double* P(int64_t off) const { return pool.d() + off * blk; }
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    CK(cudaGetDevice(&prev));
+    if (prev != dev) CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+void launch_inv(btd_plan& pl, int nbatch, const double* in, const int64_t* idx_in, int64_t add_in,
+                double* out, const int64_t* idx_out, int64_t add_out, int step, int32_t* fail_step,
+                int32_t* fail_col, DevBuf& ws, cudaStream_t st, const int64_t* fail_map = nullptr) {
+  if (nbatch <= 0) return;
+  const int mp = (int)pl.mp;
+  InvDesc d;
+  d.in = in;
+  d.idx_in = idx_in;
+  d.add_in = add_in;
+  d.out = out;
+  d.idx_out = idx_out;
+  d.add_out = add_out;
+  d.nbatch = nbatch;
+  d.m = (int)pl.m;
+  d.mp = mp;
+  d.step = step;
+  d.active_until = nullptr;
+  d.fail_step = fail_step;
+  d.fail_col = fail_col;
+  d.fail_map = fail_map;
+  d.rcond = 1e-13;  // ref _kernels.pyx:19
+  const size_t wbytes = (size_t)mp * 2 * mp * sizeof(double);
+  const int use_smem = mp <= 64;
+  int grid = std::min(nbatch, 65535);
+  if (!use_smem) {
+    const size_t want = std::min<size_t>((size_t)nbatch, std::max<size_t>(1, (size_t)(4ull << 30) / wbytes));
+    const size_t have = ws.bytes / wbytes;
+    if (have < std::min<size_t>(want, 296)) ws.alloc(std::min<size_t>(want, 296) * wbytes);
+    grid = (int)std::min<size_t>((size_t)grid, ws.bytes / wbytes);
+  }
+  d.ws = ws.d();
+  const int nt = mp <= 16 ? 128 : (mp <= 64 ? 256 : 512);
+  const size_t smem = use_smem ? wbytes : 0;
+  if (use_smem && smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(gj_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  gj_inverse_kernel<<<grid, nt, smem, st>>>(d, use_smem);
+  CK_LAUNCH();
+}
+
+// ---------------------------------------------------------------- chain kernels
+template <int MP, int KT, int WR, int WC>
+void launch_chain_t(const ChainArgs& a, bool fwd, cudaStream_t st) {
+  using Cfg = ChainCfg<MP, KT, WR, WC>;
+  const size_t smem = (size_t)(fwd ? 3 : 2) * MP * Cfg::LD * sizeof(double);
+  const int64_t ntile = (a.K + KT - 1) / KT;
+  dim3 grid((unsigned)ntile, (unsigned)a.nr);
+  if (fwd) {
+    if (smem > 48 * 1024)
+      CK(cudaFuncSetAttribute(chain_fwd_kernel<MP, KT, WR, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
+    chain_fwd_kernel<MP, KT, WR, WC><<<grid, Cfg::NT, smem, st>>>(a);
+  } else {
+    if (smem > 48 * 1024)
+      CK(cudaFuncSetAttribute(chain_bwd_kernel<MP, KT, WR, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
+    chain_bwd_kernel<MP, KT, WR, WC><<<grid, Cfg::NT, smem, st>>>(a);
+  }
+  CK_LAUNCH();
+}
+
+void launch_chain(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
+  switch (mp) {
+    case 8: launch_chain_t<8, 32, 1, 4>(a, fwd, st); break;
+    case 16: launch_chain_t<16, 16, 1, 1>(a, fwd, st); break;
+    case 32: launch_chain_t<32, 32, 2, 2>(a, fwd, st); break;
+    case 64: launch_chain_t<64, 64, 4, 2>(a, fwd, st); break;
+    case 128: launch_chain_t<128, 32, 8, 1>(a, fwd, st); break;
+    case 256: launch_chain_t<256, 32, 8, 1>(a, fwd, st); break;
+    default: fail(BTD_ERR_UNSUPPORTED, "no chain kernel for this block order");
+  }
+}
+
+int64_t pad_order(int64_t m, int mode) {
+  if (mode == 1) return (m + 7) / 8 * 8;
+  for (int64_t c : {8, 16, 32, 64, 128, 256})
+    if (m <= c) return c;
+  return (m + 7) / 8 * 8;
+}
+
+// ---------------------------------------------------------------- plan build
+void build_plan(btd_plan& pl, const double* diag, const double* lower, const double* upper, int flags,
+                cudaStream_t st, int64_t* err_row) {
+  const int64_t n = pl.n, m = pl.m;
+  int forced = -1;
+  if (const char* e = getenv("BTD_FORCE_MODE")) forced = atoi(e);
+  pl.mode = forced >= 0 ? forced : (m > 256 ? 1 : 0);
+  pl.mp = pad_order(m, pl.mode);
+  const int64_t mp = pl.mp, blk = mp * mp;
+  pl.blk = blk;
+  pl.nr = std::min<int64_t>(n, pl.ranks * std::max<int64_t>(1, pl.split));
+  pl.L = (n + pl.nr - 1) / pl.nr;
+  pl.npad = pl.L * pl.nr;
+  pl.cap = pl.L - 1;
+  const int64_t nr = pl.nr, L = pl.L, npad = pl.npad, cap = pl.cap;
+  pl.lo.resize(nr);
+  pl.slot0.resize(nr);
+  pl.nint.resize(nr);
+  pl.nlive = 0;
+  for (int64_t q = 0; q < nr; ++q) {
+    pl.lo[q] = q * L;
+    pl.slot0[q] = q * cap;
+    pl.nint[q] = (int32_t)std::max<int64_t>(0, std::min<int64_t>(L - 1, n - q * L - 1));
+    if (q * L < n) pl.nlive++;
+  }
+  pl.d_lo = pl.upload(pl.lo);
+  pl.d_slot0 = pl.upload(pl.slot0);
+  pl.d_nint = pl.upload(pl.nint);
+  std::vector<int64_t> iota(nr + 1);
+  for (int64_t i = 0; i <= nr; ++i) iota[i] = i;
+  pl.d_qiota = pl.upload(iota);
+
+  // ---- padded matrix: [C (npad) | Lw (npad) | Uw (npad)] blocks
+  DevBuf mat, tmp;
+  mat.alloc((size_t)3 * npad * blk * sizeof(double));
+  {
+    const double* srcs[3] = {diag, lower, upper};
+    const int64_t counts[3] = {n, n - 1, n - 1};
+    const bool on_dev = flags & BTD_MATRIX_ON_DEVICE;
+    size_t maxb = (size_t)n * m * m * sizeof(double);
+    if (!on_dev) tmp.alloc(maxb);
+    for (int s = 0; s < 3; ++s) {
+      const double* src = srcs[s];
+      const size_t bytes = (size_t)counts[s] * m * m * sizeof(double);
+      if (!on_dev && bytes) {
+        CK(cudaMemcpyAsync(tmp.p, src, bytes, cudaMemcpyHostToDevice, st));
+        src = tmp.d();
+      }
+      pad_blocks_kernel<<<1184, 256, 0, st>>>(src, counts[s], (int)m, mat.d() + (size_t)s * npad * blk, npad,
+                                             (int)mp, s == 0);
+      CK_LAUNCH();
+      if (!on_dev) CK(cudaStreamSynchronize(st));  // tmp reused
+    }
+  }
+  tmp.release();
+  const double* Cm = mat.d();
+  const int64_t offL = npad, offU = 2 * npad;
+
+  // ---- pool layout
+  const int64_t nslot = nr * cap;
+  int64_t o = 0;
+  auto take = [&](int64_t cnt) { int64_t r = o; o += cnt; return r; };
+  pl.off_AD = take(nslot);
+  pl.off_Dinv = take(nslot);
+  pl.off_S = take(nslot);
+  pl.off_G = take(nslot);
+  pl.off_Tb = take(nslot);
+  pl.off_Fc = take(nr);
+  pl.off_Bif = take(nr);
+  pl.off_BU = take(nr);
+  pl.off_BV = take(nr);
+  pl.off_Dt = take(nr);
+  pl.off_Rd = take(nr);
+  pl.off_Rl = take(nr);
+  pl.off_Ru = take(nr);
+  pl.off_RdT = take(nr);
+  pl.off_RlT = take(nr);
+  pl.off_RuT = take(nr);
+  pl.off_Z = take(1);
+  pl.off_I = take(1);
+  pl.pool.alloc((size_t)o * blk * sizeof(double));
+  CK(cudaMemsetAsync(pl.pool.p, 0, (size_t)o * blk * sizeof(double), st));
+  set_identity_kernel<<<64, 256, 0, st>>>(pl.P(pl.off_I), (int)mp);
+  CK_LAUNCH();
+  pl.factor_bytes = (int64_t)o * blk * sizeof(double);
+
+  double* pool = pl.pool.d();
+  const int64_t* lo_arr = pl.d_lo;
+  const int64_t* slot_arr = pl.d_slot0;
+  DevBuf ws, fail_step, fail_col;
+  fail_step.alloc(sizeof(int32_t) * std::max<int64_t>(nr, 1));
+  fail_col.alloc(sizeof(int32_t) * std::max<int64_t>(nr, 1));
+  CK(cudaMemsetAsync(fail_step.p, 0xff, sizeof(int32_t) * nr, st));
+
+  // Bif_q = upper[lo_q], Fc_q = lower[hi_q - 1]  (padded arrays; zero past n)
+  {
+    std::vector<int64_t> src(2 * nr), dst(2 * nr);
+    for (int64_t q = 0; q < nr; ++q) {
+      src[q] = offU + pl.lo[q];
+      dst[q] = pl.off_Bif + q;
+      src[nr + q] = offL + (q + 1) * L - 1;
+      dst[nr + q] = pl.off_Fc + q;
+    }
+    const int64_t* s_ = pl.upload(src);
+    const int64_t* d_ = pl.upload(dst);
+    launch_gemm(mp, mp, (int)(2 * nr), mk(pool, d_, 0, blk, mp), mk(Cm, s_, 0, blk, mp), 1.0, {}, st);
+  }
+
+  if (cap > 0) {
+    std::vector<int64_t> sa_c(2 * nr), sa_a(2 * nr), sa_b(2 * nr), gt_c(2 * nr), gt_a0(2 * nr),
+        gt_a(2 * nr), gt_b(2 * nr);
+    for (int64_t q = 0; q < nr; ++q) {
+      const int64_t s0 = pl.slot0[q];
+      sa_c[q] = pl.off_S + s0;
+      sa_c[nr + q] = pl.off_AD + s0;
+      sa_a[q] = sa_a[nr + q] = pl.off_Dinv + s0;
+      sa_b[q] = offU + pl.lo[q] + 1;   // B_g = upper[g], g = lo+1+j
+      sa_b[nr + q] = offL + pl.lo[q];  // A_g = lower[g-1]
+      gt_c[q] = pl.off_G + s0;
+      gt_c[nr + q] = pl.off_Tb + s0;
+      gt_a0[q] = pl.off_AD + s0;       // G_0 = AD_0
+      gt_a0[nr + q] = pl.off_Bif + q;  // Tb_0 = B_lo
+      gt_a[q] = pl.off_AD + s0;        // G_j = AD_j G_{j-1}
+      gt_a[nr + q] = pl.off_Tb + s0 - 1;  // Tb_j = Tb_{j-1} S_{j-1}
+      gt_b[q] = pl.off_G + s0 - 1;
+      gt_b[nr + q] = pl.off_S + s0 - 1;
+    }
+    const int64_t *d_sa_c = pl.upload(sa_c), *d_sa_a = pl.upload(sa_a), *d_sa_b = pl.upload(sa_b),
+                  *d_gt_c = pl.upload(gt_c), *d_gt_a0 = pl.upload(gt_a0), *d_gt_a = pl.upload(gt_a),
+                  *d_gt_b = pl.upload(gt_b);
+    const int nb = (int)nr;
+    for (int64_t j = 0; j < cap; ++j) {
+      // D_j = C_g - A_g S_{j-1}     (ref _kernels.pyx:168)
+      if (j == 0)
+        launch_gemm(mp, mp, nb, mk(pool, nullptr, pl.off_Dt, blk, mp), mk(Cm, lo_arr, 1, blk, mp), 1.0, {}, st);
+      else
+        launch_gemm(mp, mp, nb, mk(pool, nullptr, pl.off_Dt, blk, mp), mk(Cm, lo_arr, 1 + j, blk, mp), 1.0,
+                    {term(mk(Cm, lo_arr, offL + j, blk, mp), mk(pool, slot_arr, pl.off_S + j - 1, blk, mp), mp,
+                          -1.0)},
+                    st);
+      launch_inv(pl, nb, pool, nullptr, pl.off_Dt, pool, slot_arr, pl.off_Dinv + j, (int)j, fail_step.i32(),
+                 fail_col.i32(), ws, st);
+      // S_j = Dinv_j B_g ; AD_j = Dinv_j A_g
+      launch_gemm(mp, mp, 2 * nb, mk(pool, d_sa_c, j, blk, mp), none(), 0.0,
+                  {term(mk(pool, d_sa_a, j, blk, mp), mk(Cm, d_sa_b, j, blk, mp), mp)}, st);
+      // G_j, Tb_j
+      if (j == 0)
+        launch_gemm(mp, mp, 2 * nb, mk(pool, d_gt_c, 0, blk, mp), mk(pool, d_gt_a0, 0, blk, mp), 1.0, {}, st);
+      else
+        launch_gemm(mp, mp, 2 * nb, mk(pool, d_gt_c, j, blk, mp), none(), 0.0,
+                    {term(mk(pool, d_gt_a, j, blk, mp), mk(pool, d_gt_b, j, blk, mp), mp)}, st);
+      // BU_q += Tb_j G_j   (= B_lo U[1], ref dichotomy.py:232)
+      launch_gemm(mp, mp, nb, mk(pool, nullptr, pl.off_BU, blk, mp),
+                  j == 0 ? none() : mk(pool, nullptr, pl.off_BU, blk, mp), 1.0,
+                  {term(mk(pool, slot_arr, pl.off_Tb + j, blk, mp), mk(pool, slot_arr, pl.off_G + j, blk, mp), mp)},
+                  st);
+    }
+    // BV_q = Tb_{L-2} S_{L-2}  (= B_lo V[1])
+    launch_gemm(mp, mp, nb, mk(pool, nullptr, pl.off_BV, blk, mp), none(), 0.0,
+                {term(mk(pool, slot_arr, pl.off_Tb + cap - 1, blk, mp), mk(pool, slot_arr, pl.off_S + cap - 1, blk, mp),
+                      mp)},
+                st);
+  }
+
+  // ---- range failures: first range (in order) wins, row local to its interior
+  {
+    std::vector<int32_t> fs(nr);
+    CK(cudaMemcpyAsync(fs.data(), fail_step.p, sizeof(int32_t) * nr, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int64_t q = 0; q < nr; ++q)
+      if (fs[q] >= 0) {
+        *err_row = fs[q];
+        char buf[160];
+        snprintf(buf, sizeof buf, "block row %d: singular pivot (range %lld)", fs[q], (long long)q);
+        fail(BTD_ERR_SINGULAR_PIVOT, buf);
+      }
+  }
+
+  // ---- reduced system (ref dichotomy.py:212-236)
+  {
+    std::vector<int64_t> rd_c(nr), rd_in(nr), t1a(nr), t1b(nr), t2a(nr), rl_c, rl_a, rl_b, ru_c, ru_a;
+    for (int64_t q = 0; q < nr; ++q) {
+      rd_c[q] = pl.off_Rd + q;
+      rd_in[q] = pl.lo[q];
+      t1a[q] = q >= 1 ? pl.off_Fc + q - 1 : pl.off_Z;
+      t1b[q] = (q >= 1 && cap > 0) ? pl.off_S + pl.slot0[q - 1] + cap - 1 : pl.off_Z;
+      t2a[q] = pl.off_BU + q;
+      if (q >= 1) {
+        rl_c.push_back(pl.off_Rl + q - 1);
+        rl_a.push_back(pl.off_Fc + q - 1);
+        rl_b.push_back(cap > 0 ? pl.off_G + pl.slot0[q - 1] + cap - 1 : pl.off_I);
+      }
+      if (q <= nr - 2) {
+        ru_c.push_back(pl.off_Ru + q);
+        ru_a.push_back(cap > 0 ? pl.off_BV + q : pl.off_Bif + q);
+      }
+    }
+    launch_gemm(mp, mp, (int)nr, mk(pool, pl.upload(rd_c), 0, blk, mp), mk(Cm, pl.upload(rd_in), 0, blk, mp), 1.0,
+                {term(mk(pool, pl.upload(t1a), 0, blk, mp), mk(pool, pl.upload(t1b), 0, blk, mp), mp, -1.0),
+                 term(mk(pool, pl.upload(t2a), 0, blk, mp), mk(pool + pl.off_I * blk, nullptr, 0, 0, mp), mp, -1.0)},
+                st);
+    if (!rl_c.empty()) {
+      launch_gemm(mp, mp, (int)rl_c.size(), mk(pool, pl.upload(rl_c), 0, blk, mp), none(), 0.0,
+                  {term(mk(pool, pl.upload(rl_a), 0, blk, mp), mk(pool, pl.upload(rl_b), 0, blk, mp), mp)}, st);
+      launch_gemm(mp, mp, (int)ru_c.size(), mk(pool, pl.upload(ru_c), 0, blk, mp),
+                  mk(pool, pl.upload(ru_a), 0, blk, mp), 1.0, {}, st);
+    }
+    // transposed system T = R^T: diag Rd^T, lower Ru^T, upper Rl^T (ref core.py:137-143)
+    std::vector<int64_t> ti, to;
+    for (int64_t q = 0; q < nr; ++q) {
+      ti.push_back(pl.off_Rd + q); to.push_back(pl.off_RdT + q);
+      if (q + 1 < nr) {
+        ti.push_back(pl.off_Rl + q); to.push_back(pl.off_RlT + q);
+        ti.push_back(pl.off_Ru + q); to.push_back(pl.off_RuT + q);
+      }
+    }
+    const int nb = (int)ti.size();
+    dim3 grid((unsigned)((mp + 31) / 32), (unsigned)((mp + 31) / 32), std::min(nb, 65535));
+    transpose_blocks_kernel<<<grid, dim3(32, 8), 0, st>>>(pool, pl.upload(ti), pool, pl.upload(to), nb, (int)mp);
+    CK_LAUNCH();
+  }
+  mat.release();
+
+  // ---- partition tree inverse rows (ref dichotomy.py:134-146, 298-304)
+  pl.nodes = partition_tree(nr, &pl.depth);
+  const int nn = (int)pl.nodes.size();
+  std::vector<int64_t> nb0(nn), sz(nn), roff(nn), rld(nn), eoff(nn + 1);
+  int64_t tot = 0, rtot = 0;
+  int64_t maxlevel = 0;
+  for (int b = 0; b < nn; ++b) {
+    sz[b] = pl.nodes[b].hi - pl.nodes[b].lo + 1;
+    nb0[b] = tot;
+    tot += sz[b];
+    roff[b] = rtot;
+    rld[b] = sz[b] * mp;
+    eoff[b] = rtot;
+    rtot += sz[b] * blk;
+    maxlevel = std::max(maxlevel, pl.nodes[b].level);
+  }
+  eoff[nn] = rtot;
+  // tree pool: Dp, Sp, ADp, Y (tot each) + Dt scratch (nn)
+  DevBuf tp, tfs, tfc;
+  const int64_t tpD = 0, tpS = tot, tpAD = 2 * tot, tpY = 3 * tot, tpDt = 4 * tot;
+  tp.alloc((size_t)(4 * tot + nn) * blk * sizeof(double));
+  CK(cudaMemsetAsync(tp.p, 0, (size_t)(4 * tot + nn) * blk * sizeof(double), st));
+  tfs.alloc(sizeof(int32_t) * nn);
+  tfc.alloc(sizeof(int32_t) * nn);
+  CK(cudaMemsetAsync(tfs.p, 0xff, sizeof(int32_t) * nn, st));
+  double* T = tp.d();
+  for (int64_t lev = 0; lev <= maxlevel; ++lev) {
+    std::vector<int> ids;
+    int64_t smax = 0;
+    for (int b = 0; b < nn; ++b)
+      if (pl.nodes[b].level == lev) { ids.push_back(b); smax = std::max(smax, sz[b]); }
+    // factor D'_i, S'_i, AD'_i for i = 0..smax-1 (transposed system, batched over nodes)
+    for (int64_t i = 0; i < smax; ++i) {
+      std::vector<int64_t> dt_c, dt_in, dt_a, dt_b, inv_in, inv_out, sc, sa, sb, ac, aa, ab;
+      std::vector<int64_t> failidx;
+      for (int b : ids) {
+        if (sz[b] <= i) continue;
+        const int64_t lo = pl.nodes[b].lo;
+        dt_c.push_back(tpDt + b);
+        dt_in.push_back(pl.off_RdT + lo + i);
+        dt_a.push_back(i >= 1 ? pl.off_RuT + lo + i - 1 : pl.off_Z);
+        dt_b.push_back(i >= 1 ? tpS + nb0[b] + i - 1 : -1);
+        inv_in.push_back(tpDt + b);
+        inv_out.push_back(tpD + nb0[b] + i);
+        failidx.push_back(b);
+        if (i + 1 < sz[b]) {  // S'_i = D'^{-1}_i T.upper = D'^{-1} Rl^T_{lo+i}
+          sc.push_back(tpS + nb0[b] + i); sa.push_back(tpD + nb0[b] + i); sb.push_back(pl.off_RlT + lo + i);
+        }
+        if (i >= 1) {  // AD'_i = D'^{-1}_i T.lower[i-1] = D'^{-1} Ru^T_{lo+i-1}
+          ac.push_back(tpAD + nb0[b] + i); aa.push_back(tpD + nb0[b] + i); ab.push_back(pl.off_RuT + lo + i - 1);
+        }
+      }
+      const int cnt = (int)dt_c.size();
+      // D'_i into tree-pool scratch; operands from two pools -> stage via pool copy when i >= 1
+      if (i == 0) {
+        launch_gemm(mp, mp, cnt, mk(T, pl.upload(dt_c), 0, blk, mp), mk(pool, pl.upload(dt_in), 0, blk, mp), 1.0, {},
+                    st);
+      } else {
+        launch_gemm(mp, mp, cnt, mk(T, pl.upload(dt_c), 0, blk, mp), mk(pool, pl.upload(dt_in), 0, blk, mp), 1.0,
+                    {term(mk(pool, pl.upload(dt_a), 0, blk, mp), mk(T, pl.upload(dt_b), 0, blk, mp), mp, -1.0)}, st);
+      }
+      launch_inv(pl, cnt, T, pl.upload(inv_in), 0, T, pl.upload(inv_out), 0, (int)i, tfs.i32(), tfc.i32(), ws, st,
+                 pl.upload(failidx));
+      if (!sc.empty())
+        launch_gemm(mp, mp, (int)sc.size(), mk(T, pl.upload(sc), 0, blk, mp), none(), 0.0,
+                    {term(mk(T, pl.upload(sa), 0, blk, mp), mk(pool, pl.upload(sb), 0, blk, mp), mp)}, st);
+      if (!ac.empty())
+        launch_gemm(mp, mp, (int)ac.size(), mk(T, pl.upload(ac), 0, blk, mp), none(), 0.0,
+                    {term(mk(T, pl.upload(aa), 0, blk, mp), mk(pool, pl.upload(ab), 0, blk, mp), mp)}, st);
+    }
+    // forward solve with unit RHS at kk = k - lo: y_kk = D'^{-1}_kk ; y_i = AD'_i y_{i-1}
+    for (int64_t i = 0; i < smax; ++i) {
+      std::vector<int64_t> cc, ci, gc, ga, gb;
+      for (int b : ids) {
+        const int64_t kk = pl.nodes[b].k - pl.nodes[b].lo;
+        if (i >= sz[b]) continue;
+        if (i == kk) { cc.push_back(tpY + nb0[b] + i); ci.push_back(tpD + nb0[b] + i); }
+        else if (i > kk) { gc.push_back(tpY + nb0[b] + i); ga.push_back(tpAD + nb0[b] + i); gb.push_back(tpY + nb0[b] + i - 1); }
+      }
+      if (!cc.empty())
+        launch_gemm(mp, mp, (int)cc.size(), mk(T, pl.upload(cc), 0, blk, mp), mk(T, pl.upload(ci), 0, blk, mp), 1.0, {},
+                    st);
+      if (!gc.empty())
+        launch_gemm(mp, mp, (int)gc.size(), mk(T, pl.upload(gc), 0, blk, mp), none(), 0.0,
+                    {term(mk(T, pl.upload(ga), 0, blk, mp), mk(T, pl.upload(gb), 0, blk, mp), mp)}, st);
+    }
+    // backward: y_i += S'_i y_{i+1}
+    for (int64_t i = smax - 2; i >= 0; --i) {
+      std::vector<int64_t> c, a, bb;
+      for (int b : ids) {
+        if (i + 1 >= sz[b]) continue;
+        c.push_back(tpY + nb0[b] + i); a.push_back(tpS + nb0[b] + i); bb.push_back(tpY + nb0[b] + i + 1);
+      }
+      if (!c.empty()) {
+        const int64_t* dc = pl.upload(c);
+        launch_gemm(mp, mp, (int)c.size(), mk(T, dc, 0, blk, mp), mk(T, dc, 0, blk, mp), 1.0,
+                    {term(mk(T, pl.upload(a), 0, blk, mp), mk(T, pl.upload(bb), 0, blk, mp), mp)}, st);
+      }
+    }
+  }
+  // tree failures: first node in BFS order
+  {
+    std::vector<int32_t> fs(nn);
+    CK(cudaMemcpyAsync(fs.data(), tfs.p, sizeof(int32_t) * nn, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int b = 0; b < nn; ++b)
+      if (fs[b] >= 0) {
+        *err_row = fs[b];
+        char buf[160];
+        snprintf(buf, sizeof buf, "block row %d: singular pivot (reduced system, tree node %d)", fs[b], b);
+        fail(BTD_ERR_SINGULAR_PIVOT, buf);
+      }
+  }
+  // R rows, then E = R[:, :mp] Rl_{lo-1}, H = R[:, -mp:] Ru_{hi}
+  pl.Rrows.alloc((size_t)rtot * sizeof(double));
+  {
+    std::vector<int64_t> ynb0(nn);
+    for (int b = 0; b < nn; ++b) ynb0[b] = tpY + nb0[b];
+    assemble_rows_kernel<<<1184, 256, 0, st>>>(T, pl.upload(ynb0), pl.upload(roff), pl.upload(sz), pl.upload(eoff), nn,
+                                              rtot, (int)mp, pl.Rrows.d());
+    CK_LAUNCH();
+  }
+  pl.d_roff = pl.upload(roff);
+  pl.d_rld = pl.upload(rld);
+  pl.EH.alloc((size_t)2 * nn * blk * sizeof(double));
+  CK(cudaMemsetAsync(pl.EH.p, 0, (size_t)2 * nn * blk * sizeof(double), st));
+  {
+    std::vector<int64_t> ec, ea, eld, eb, hc, ha, hld, hb;
+    for (int b = 0; b < nn; ++b) {
+      const Node& nd = pl.nodes[b];
+      if (nd.lo >= 1) { ec.push_back(2 * b); ea.push_back(roff[b]); eld.push_back(rld[b]); eb.push_back(pl.off_Rl + nd.lo - 1); }
+      if (nd.hi <= nr - 2) {
+        hc.push_back(2 * b + 1); ha.push_back(roff[b] + (sz[b] - 1) * mp); hld.push_back(rld[b]);
+        hb.push_back(pl.off_Ru + nd.hi);
+      }
+    }
+    if (!ec.empty())
+      launch_gemm(mp, mp, (int)ec.size(), mk(pl.EH.d(), pl.upload(ec), 0, blk, mp), none(), 0.0,
+                  {term(mk(pl.Rrows.d(), pl.upload(ea), 0, 1, 0, pl.upload(eld)), mk(pool, pl.upload(eb), 0, blk, mp), mp)},
+                  st);
+    if (!hc.empty())
+      launch_gemm(mp, mp, (int)hc.size(), mk(pl.EH.d(), pl.upload(hc), 0, blk, mp), none(), 0.0,
+                  {term(mk(pl.Rrows.d(), pl.upload(ha), 0, 1, 0, pl.upload(hld)), mk(pool, pl.upload(hb), 0, blk, mp), mp)},
+                  st);
+  }
+  // solve-time level batches
+  {
+    std::vector<int64_t> nlo(nn);
+    for (int b = 0; b < nn; ++b) nlo[b] = pl.nodes[b].lo;
+    pl.d_nlo = pl.upload(nlo);
+    pl.levels.resize(maxlevel + 1);
+    for (int64_t lev = 0; lev <= maxlevel; ++lev) {
+      std::vector<int64_t> c, z, e, xl, h, xh;
+      for (int b = 0; b < nn; ++b) {
+        const Node& nd = pl.nodes[b];
+        if (nd.level != lev) continue;
+        c.push_back(nd.k); z.push_back(b); e.push_back(2 * b); h.push_back(2 * b + 1);
+        xl.push_back(nd.lo >= 1 ? nd.lo - 1 : nr);
+        xh.push_back(nd.hi + 1 <= nr - 1 ? nd.hi + 1 : nr);
+      }
+      auto& L_ = pl.levels[lev];
+      L_.count = (int)c.size();
+      L_.c_idx = pl.upload(c); L_.z_idx = pl.upload(z); L_.e_idx = pl.upload(e);
+      L_.xl_idx = pl.upload(xl); L_.h_idx = pl.upload(h); L_.xh_idx = pl.upload(xh);
+    }
+    // interface RHS carry: f~_q += Fc_{q-1} y_{q-1,last} for ranges q-1 entirely inside [0,n)
+    std::vector<int64_t> cq, cf, cr;
+    for (int64_t q = 1; q < nr; ++q)
+      if (cap > 0 && pl.lo[q] <= n && pl.nint[q - 1] == cap) {
+        cq.push_back(q); cf.push_back(pl.off_Fc + q - 1); cr.push_back(pl.lo[q] - 1);
+      }
+    pl.ncarry = (int)cq.size();
+    pl.carry_q = pl.upload(cq); pl.carry_fc = pl.upload(cf); pl.carry_row = pl.upload(cr);
+    // mode-1 step batches
+    if (pl.mode == 1) {
+      pl.steps1.resize(cap);
+      for (int64_t j = 0; j < cap; ++j) {
+        std::vector<int64_t> xr, xs, xq, tr, ts, tq;
+        int cnt = 0;
+        for (int64_t q = 0; q < nr; ++q) {
+          if (pl.nint[q] > j) ++cnt;
+          if (j < pl.nint[q] - 1) { xr.push_back(pl.lo[q] + 1 + j); xs.push_back(pl.slot0[q] + j); xq.push_back(q); }
+          else if (j == pl.nint[q] - 1) { tr.push_back(pl.lo[q] + 1 + j); ts.push_back(pl.slot0[q] + j); tq.push_back(q); }
+        }
+        auto& s = pl.steps1[j];
+        s.cnt = cnt; s.nx = (int)xq.size(); s.nt = (int)tq.size();
+        s.x_row = pl.upload(xr); s.x_slot = pl.upload(xs); s.x_q = pl.upload(xq);
+        s.t_row = pl.upload(tr); s.t_slot = pl.upload(ts); s.t_q = pl.upload(tq);
+      }
+    }
+  }
+  CK(cudaStreamSynchronize(st));
+  pl.factor_bytes += (int64_t)(rtot + 2 * nn * blk) * sizeof(double);
+}
+
+// ---------------------------------------------------------------- solve
+void ensure_scratch(btd_plan& pl, int64_t K) {
+  if (pl.scratch_k == K) return;
+  const int64_t mpK = pl.mp * K;
+  pl.base.alloc((size_t)pl.nr * mpK * sizeof(double));
+  pl.zbuf.alloc((size_t)pl.nodes.size() * mpK * sizeof(double));
+  pl.xt.alloc((size_t)(pl.nr + 1) * mpK * sizeof(double));
+  CK(cudaMemset(pl.xt.p, 0, (size_t)(pl.nr + 1) * mpK * sizeof(double)));
+  CK(cudaMemset(pl.base.p, 0, (size_t)pl.nr * mpK * sizeof(double)));
+  pl.scratch_k = K;
+}
+
+void solve_device(btd_plan& pl, const double* F, double* X, int64_t K, cudaStream_t st) {
+  const int64_t mp = pl.mp, m = pl.m, blk = pl.blk, nr = pl.nr;
+  const int64_t mpK = mp * K, mK = m * K;
+  double* pool = pl.pool.d();
+  double* base = pl.base.d();
+  double* xt = pl.xt.d();
+  double* z = pl.zbuf.d();
+  if (pl.mode == 0) {
+    ChainArgs a;
+    a.lo = pl.d_lo; a.nint = pl.d_nint; a.slot0 = pl.d_slot0; a.nr = (int)nr;
+    a.m = (int)m; a.n = pl.n; a.K = K; a.F = F; a.X = X;
+    a.AD = pool + pl.off_AD * blk; a.Dinv = pool + pl.off_Dinv * blk; a.Tb = pool + pl.off_Tb * blk;
+    a.S = pool + pl.off_S * blk; a.G = pool + pl.off_G * blk;
+    a.base = base; a.xt = xt;
+    launch_chain(mp, a, true, st);
+  } else {
+    // mode 1: base_q = F[lo_q] (rows < m; pad rows stay 0), then one GEMM launch per row step
+    launch_gemm(m, K, pl.nlive, mk(base, nullptr, 0, mpK, K), mk(F, pl.d_lo, 0, mK, K), 1.0, {}, st);
+    for (int64_t j = 0; j < pl.cap; ++j) {
+      const auto& s = pl.steps1[j];
+      if (s.cnt == 0) break;
+      if (j == 0)
+        launch_gemm(m, K, s.cnt, mk(X, pl.d_lo, 1, mK, K), none(), 0.0,
+                    {term(mk(pool, pl.d_slot0, pl.off_Dinv, blk, mp), mk(F, pl.d_lo, 1, mK, K), m)}, st);
+      else
+        launch_gemm(m, K, s.cnt, mk(X, pl.d_lo, 1 + j, mK, K), none(), 0.0,
+                    {term(mk(pool, pl.d_slot0, pl.off_Dinv + j, blk, mp), mk(F, pl.d_lo, 1 + j, mK, K), m),
+                     term(mk(pool, pl.d_slot0, pl.off_AD + j, blk, mp), mk(X, pl.d_lo, j, mK, K), m)},
+                    st);
+      launch_gemm(mp, K, s.cnt, mk(base, nullptr, 0, mpK, K), mk(base, nullptr, 0, mpK, K), 1.0,
+                  {term(mk(pool, pl.d_slot0, pl.off_Tb + j, blk, mp), mk(X, pl.d_lo, 1 + j, mK, K), m)}, st);
+    }
+  }
+  // interface RHS (ref dichotomy.py:239-276): f~_q = base_q + Fc_{q-1} y_{q-1,last}
+  launch_gemm(mp, K, pl.ncarry, mk(base, pl.carry_q, 0, mpK, K), mk(base, pl.carry_q, 0, mpK, K), 1.0,
+              {term(mk(pool, pl.carry_fc, 0, blk, mp), mk(X, pl.carry_row, 0, mK, K), m)}, st);
+  // Algorithm 1: z_node = R_node f~[lo..hi]  (all nodes, one launch)
+  const int nn = (int)pl.nodes.size();
+  {
+    // k per node = size*mp == rld
+    launch_gemm(mp, K, nn, mk(z, nullptr, 0, mpK, K), none(), 0.0,
+                {term(mk(pl.Rrows.d(), pl.d_roff, 0, 1, 0, pl.d_rld), mk(base, pl.d_nlo, 0, mpK, K), 0, 1.0, pl.d_rld)},
+                st);
+  }
+  for (const auto& lev : pl.levels) {
+    launch_gemm(mp, K, lev.count, mk(xt, lev.c_idx, 0, mpK, K), mk(z, lev.z_idx, 0, mpK, K), 1.0,
+                {term(mk(pl.EH.d(), lev.e_idx, 0, blk, mp), mk(xt, lev.xl_idx, 0, mpK, K), mp),
+                 term(mk(pl.EH.d(), lev.h_idx, 0, blk, mp), mk(xt, lev.xh_idx, 0, mpK, K), mp)},
+                st);
+  }
+  if (pl.mode == 0) {
+    ChainArgs a;
+    a.lo = pl.d_lo; a.nint = pl.d_nint; a.slot0 = pl.d_slot0; a.nr = (int)nr;
+    a.m = (int)m; a.n = pl.n; a.K = K; a.F = F; a.X = X;
+    a.AD = pool + pl.off_AD * blk; a.Dinv = pool + pl.off_Dinv * blk; a.Tb = pool + pl.off_Tb * blk;
+    a.S = pool + pl.off_S * blk; a.G = pool + pl.off_G * blk;
+    a.base = base; a.xt = xt;
+    launch_chain(mp, a, false, st);
+  } else {
+    // x[lo_q] = x~_q
+    launch_gemm(m, K, pl.nlive, mk(X, pl.d_lo, 0, mK, K), mk(xt, nullptr, 0, mpK, K), 1.0, {}, st);
+    for (int64_t j = pl.cap - 1; j >= 0; --j) {
+      const auto& s = pl.steps1[j];
+      // x_j = y_j + G_j x~_q + S_j x_{j+1}   (x_{j+1} an interior row)
+      launch_gemm(m, K, s.nx, mk(X, s.x_row, 0, mK, K), mk(X, s.x_row, 0, mK, K), 1.0,
+                  {term(mk(pool, s.x_slot, pl.off_G, blk, mp), mk(xt, s.x_q, 0, mpK, K), mp),
+                   term(mk(pool, s.x_slot, pl.off_S, blk, mp), mk(X, s.x_row, 1, mK, K), m)},
+                  st);
+      // last interior row: x_{j+1} = x~_{q+1}
+      launch_gemm(m, K, s.nt, mk(X, s.t_row, 0, mK, K), mk(X, s.t_row, 0, mK, K), 1.0,
+                  {term(mk(pool, s.t_slot, pl.off_G, blk, mp), mk(xt, s.t_q, 0, mpK, K), mp),
+                   term(mk(pool, s.t_slot, pl.off_S, blk, mp), mk(xt, s.t_q, 1, mpK, K), mp)},
+                  st);
+    }
+  }
+}
+
+}  // namespace
+
+// ======================================================================= C ABI
+extern "C" {
+
+int btd_version(void) { return 1; }
+int64_t btd_launch_count(void) { return g_launches.load(); }
+const char* btd_last_error(void) { return g_err.c_str(); }
+
+int btd_plan_create(const double* diag, const double* lower, const double* upper, int64_t n, int64_t m,
+                    int64_t ranks, int64_t split, int device, int flags, void* stream, btd_plan** out_plan,
+                    int64_t* err_row) {
+  g_err.clear();
+  if (err_row) *err_row = -1;
+  if (!out_plan) { g_err = "out_plan is NULL"; return BTD_ERR_INVALID_ARG; }
+  *out_plan = nullptr;
+  if (n < 1 || m < 1) { g_err = "need n >= 1 and m >= 1"; return BTD_ERR_DIMENSION; }
+  if (ranks < 1 || ranks > n) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "ranks=%lld outside [1, N=%lld]", (long long)ranks, (long long)n);
+    g_err = buf;
+    return BTD_ERR_INVALID_RANKS;  // ref dichotomy.py:326-327
+  }
+  if (!diag || (n > 1 && (!lower || !upper))) { g_err = "NULL matrix pointer"; return BTD_ERR_INVALID_ARG; }
+  auto* pl = new btd_plan();
+  pl->device = device;
+  pl->n = n; pl->m = m; pl->ranks = ranks; pl->split = std::max<int64_t>(1, split);
+  int64_t row = -1;
+  try {
+    DeviceGuard dg(device);
+    build_plan(*pl, diag, lower, upper, flags, (cudaStream_t)stream, &row);
+  } catch (const BtdError& e) {
+    if (err_row) *err_row = row;
+    delete pl;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    delete pl;
+    return BTD_ERR_CUDA;
+  }
+  *out_plan = pl;
+  return BTD_OK;
+}
+
+int btd_plan_solve(btd_plan* pl, const double* f, double* x, int64_t k, void* stream) {
+  g_err.clear();
+  if (!pl || !f || !x) { g_err = "NULL argument"; return BTD_ERR_INVALID_ARG; }
+  if (k < 1) { g_err = "k must be >= 1"; return BTD_ERR_DIMENSION; }
+  try {
+    DeviceGuard dg(pl->device);
+    std::lock_guard<std::mutex> lk(pl->mu);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (pl->last_stream != st && pl->scratch_k) CK(cudaStreamSynchronize(pl->last_stream));
+    pl->last_stream = st;
+    ensure_scratch(*pl, k);
+    solve_device(*pl, f, x, k, st);
+  } catch (const BtdError& e) {
+    return e.code;
+  }
+  return BTD_OK;
+}
+
+int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int64_t k, void* stream) {
+  g_err.clear();
+  if (!pl || !f_host || !x_host) { g_err = "NULL argument"; return BTD_ERR_INVALID_ARG; }
+  if (k < 1) { g_err = "k must be >= 1"; return BTD_ERR_DIMENSION; }
+  try {
+    DeviceGuard dg(pl->device);
+    std::lock_guard<std::mutex> lk(pl->mu);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (pl->last_stream != st && pl->scratch_k) CK(cudaStreamSynchronize(pl->last_stream));
+    pl->last_stream = st;
+    const size_t bytes = (size_t)pl->n * pl->m * k * sizeof(double);
+    if (pl->hostio_k != k) {
+      pl->hostio.alloc(bytes);
+      pl->hostio_k = k;
+    }
+    ensure_scratch(*pl, k);
+    CK(cudaMemcpyAsync(pl->hostio.p, f_host, bytes, cudaMemcpyHostToDevice, st));
+    solve_device(*pl, pl->hostio.d(), pl->hostio.d(), k, st);
+    CK(cudaMemcpyAsync(x_host, pl->hostio.p, bytes, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  } catch (const BtdError& e) {
+    return e.code;
+  }
+  return BTD_OK;
+}
+
+int btd_plan_destroy(btd_plan* pl) {
+  if (!pl) return BTD_OK;
+  {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(pl->device);
+    cudaDeviceSynchronize();
+    delete pl;
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  return BTD_OK;
+}
+
+int btd_plan_query(const btd_plan* pl, btd_plan_info* info) {
+  if (!pl || !info) return BTD_ERR_INVALID_ARG;
+  memset(info, 0, sizeof *info);
+  info->n = pl->n; info->m = pl->m; info->mp = pl->mp; info->ranks = pl->ranks; info->split = pl->split;
+  info->nranges = pl->nr; info->L = pl->L; info->tree_nodes = (int64_t)pl->nodes.size();
+  info->tree_depth = pl->depth; info->factor_bytes = pl->factor_bytes; info->row_lo = 0; info->row_hi = pl->n;
+  info->device = pl->device; info->mode = pl->mode;
+  return BTD_OK;
+}
+
+}  // extern "C"

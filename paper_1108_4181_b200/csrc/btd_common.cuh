@@ -1,0 +1,43 @@
+// Shared device helpers for the B200 dichotomy kernels (sm_100a).
+//
+// FP64 products go through the warp-level tensor-core instruction
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Measured on this pool's B200
+// (profiles/r01_fp64_rates.txt): DMMA sustains 37.2 TFLOP/s = 64 FMA/clk/SM
+// from 4 warps/SM, plain DFMA tops out at 33.5 TFLOP/s (issue-bound), cuBLAS
+// DGEMM 35.5 TFLOP/s.  tcgen05 has no f64 kind on sm_100a, so DMMA is the
+// fp64 tensor path.
+//
+// Fragment conventions for m8n8k4 (lane l, g = l>>2, t = l&3):
+//   A (8x4, row):  a = A[g][t]          B (4x8, col): b = B[t][g]
+//   C (8x8):       c0 = C[g][2t], c1 = C[g][2t+1]
+// A "pair step" covers k = 8s..8s+7 with two DMMAs: the first uses k-slots
+// {8s+2t}, the second {8s+2t+1}.  The reduction order is a permutation of k,
+// which lets every lane fetch its two A values with one 16-byte load.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define BTD_DEVINL __device__ __forceinline__
+
+BTD_DEVINL void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+BTD_DEVINL unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+BTD_DEVINL void cp_async16(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem_dst)), "l"(gmem_src));
+}
+BTD_DEVINL void cp_async8(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem_dst)), "l"(gmem_src));
+}
+BTD_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+BTD_DEVINL void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// 16B read-only streaming load of a factor fragment (L2-resident factors,
+// re-read by the CTAs that share a range; keep them out of L1).
+BTD_DEVINL double2 ldg_cg2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
