@@ -1,0 +1,441 @@
+#!/usr/bin/env python
+"""Benchmark of the many-RHS block-tridiagonal dichotomy solve (plan_solve).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl b200|reference]
+
+Metric (BASELINE.json): right-hand-side columns solved per second at a fixed
+matrix.  One *step* = one ``plan_solve`` of the config's K columns, F -> X,
+with the plan (Algorithm 2 step 1) built once beforehand and timed separately.
+Default workload: configs[1] (c1, the 2-D Laguerre acoustic strip operator,
+N=4096 x M=256 blocks, K=256), the configuration the metric is quoted on that
+fits one GPU.
+
+* ``value``: device-resident F/X, CUDA events on the solve stream around
+  exactly K steps, max over ranks.  Inputs (F 2.1 GB, factors 10.7 GB for c1)
+  are larger than the 126 MB L2, so no flush is needed between steps.
+* ``e2e``: the same metric through the reference-facing host API
+  (``btd_plan_solve_host``: pinned host F -> device -> solve -> host X).
+* ``roofline``: the dominant kernel (the fused forward sweep) -- algorithmic
+  flops (or bytes) per launch / its CUDA-event duration, against the fp64
+  tensor peak (cuBLAS DGEMM measured in this run; MEASURED_PEAKS.json has no
+  fp64 entry) or the measured HBM copy bandwidth.
+* ``cpu_baseline``: the CPU oracle (a port of the reference algorithm) on a
+  bounded sample of the same workload, scaled to full-size RHS/s.
+* ``--impl reference``: the reference algorithm on the host cores (the oracle
+  port; /root/reference cannot travel to the GPU box), same metric/config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# Per-config plan parameters.  ranks = the reference's P; split = on-device
+# second-level ranges per reference range (hard part 1).
+BENCH_CFG = {
+    "c0": dict(ranks=4, split=1, dtype="f64"),
+    "c1": dict(ranks=18, split=1, dtype="f64"),
+    "c2": dict(ranks=9, split=1, dtype="f64"),
+    "c4": dict(ranks=8, split=74, dtype="f64"),
+}
+# CPU sample per config: (block rows, columns, ranks) of the same operator family
+CPU_SAMPLE = {
+    "c0": (512, 32, 4),
+    "c1": (64, 16, 2),
+    "c2": (256, 64, 4),
+    "c4": (8192, 8, 8),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+def fp64_peak_tflops(torch):
+    """cuBLAS DGEMM 4096^3, best of 5 -- the fp64 tensor roofline denominator."""
+    n = 4096
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn_like(a)
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize()
+    best = 1e9
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(5):
+        e0.record()
+        a @ b
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2 * n ** 3 / best / 1e9
+
+
+def make_inputs(name, torch, seed=0):
+    from paper_1108_4181_b200 import configs
+
+    return configs.generate(name, device="cuda", seed=seed)
+
+
+def interior_rows(n, nranges, L):
+    tot = 0
+    for q in range(nranges):
+        lo = q * L
+        tot += max(0, min(L - 1, n - lo - 1))
+    return tot
+
+
+# --------------------------------------------------------------------------- CPU arm
+def cpu_sample_run(name, steps=1, warmup=0):
+    """Time the oracle port of the reference plan_solve on a bounded sample of
+    config `name`; returns (rhs_per_s scaled to full size, seconds, sample text)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import blocktri_oracle as O
+    from paper_1108_4181_b200 import configs
+
+    cfg = configs.CONFIGS[name]
+    ns, ks, ps = CPU_SAMPLE[name]
+    if cfg["kind"] == "strip":
+        d, lo, up, f = configs.strip_numpy(ns, cfg["m"], ks, cfg["shift"], 0)
+    else:
+        d, lo, up, f = configs.dominant_numpy(ns, cfg["m"], ks, 0)
+    plan = O.plan_build(d, lo, up, ps)
+    for _ in range(warmup):
+        O.plan_solve(plan, f)
+    ts = []
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        O.plan_solve(plan, f)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    # plan_solve is linear in N*K at fixed M: full-size RHS/s = K_s/t * N_s/N
+    value = ks / t * ns / cfg["n"]
+    sample = (f"oracle port (numpy, ref dichotomy.py:358-390) on N={ns} of {cfg['n']} block rows, "
+              f"K={ks} of {cfg['k']} columns, P={ps}; RHS/s scaled by N_s/N")
+    return value, t, sample
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    name = args.config
+    from paper_1108_4181_b200 import configs
+
+    cfg = configs.CONFIGS[name]
+    ts = []
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, t, sample = cpu_sample_run(name)
+        if i >= args.warmup:
+            ts.append(t)
+            vals.append(v)
+    value = statistics.median(vals)
+    cores = 1
+    try:
+        import threadpoolctl
+
+        cores = max(1, max((p.get("num_threads", 1) for p in threadpoolctl.threadpool_info()), default=1))
+    except Exception:
+        pass
+    line = {
+        "impl": "reference", "metric": "rhs_columns_per_second", "value": value, "unit": "RHS/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.median(ts), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy, BASELINE.json distributions)",
+        "config": {"workload": name, "n": cfg["n"], "m": cfg["m"], "k": cfg["k"], "ranks": CPU_SAMPLE[name][2]},
+        "cpu_baseline": {"value": value, "unit": "RHS/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "RHS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_b200(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1108_4181_b200 import _native, configs, plan_build_arrays
+
+    name = args.config
+    cfg = configs.CONFIGS[name]
+    bc = dict(BENCH_CFG[name])
+    if args.ranks:
+        bc["ranks"] = args.ranks
+    if args.split:
+        bc["split"] = args.split
+    n, m, K = cfg["n"], cfg["m"], cfg["k"]
+    lib = _native.load()
+
+    diag, lower, upper, F = make_inputs(name, torch)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    plan = plan_build_arrays(diag, lower, upper, bc["ranks"], split=bc["split"])
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    del diag, lower, upper
+    torch.cuda.empty_cache()
+    X = torch.empty_like(F)
+    stream = torch.cuda.current_stream()
+    sp = __import__("ctypes").c_void_p(stream.cuda_stream)
+
+    def solve():
+        st = lib.btd_plan_solve(plan.handle, __import__("ctypes").c_void_p(F.data_ptr()),
+                                __import__("ctypes").c_void_p(X.data_ptr()), K, sp)
+        if st:
+            _native.check(st)
+
+    for _ in range(args.warmup):
+        solve()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lc0 = _native.launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            solve()
+        e1.record(stream)
+        e1.synchronize()
+    launches = _native.launch_count() - lc0
+    ms = e0.elapsed_time(e1)
+    if dist:
+        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_step = ms / args.steps
+    value = world * K * args.steps / (ms / 1e3)
+
+    # per-phase timing (separate profiled pass: events between the phases)
+    lib.btd_plan_set_profiling(plan.handle, 1)
+    import ctypes
+
+    buf = (ctypes.c_double * 4)()
+    nsv = ctypes.c_int64()
+    lib.btd_plan_phase_times(plan.handle, buf, ctypes.byref(nsv), 1)
+    for _ in range(args.steps):
+        solve()
+    torch.cuda.synchronize()
+    lib.btd_plan_phase_times(plan.handle, buf, ctypes.byref(nsv), 1)
+    lib.btd_plan_set_profiling(plan.handle, 0)
+    ph = [buf[i] / max(1, nsv.value) for i in range(4)]
+
+    # correctness spot check at full size: relative residual of one solve
+    res = None
+    if not args.no_check:
+        res = residual_check(torch, name, X, F, configs)
+
+    # e2e through the host API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        Fh = F.cpu().pin_memory()
+        Xh = torch.empty_like(Fh).pin_memory()
+        del X
+        torch.cuda.empty_cache()
+
+        def solve_host():
+            st = lib.btd_plan_solve_host(plan.handle, ctypes.c_void_p(Fh.data_ptr()), ctypes.c_void_p(Xh.data_ptr()),
+                                         K, sp)
+            if st:
+                _native.check(st)
+
+        solve_host()
+        torch.cuda.synchronize()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        esteps = max(1, min(args.steps, 5))
+        h0.record(stream)
+        for _ in range(esteps):
+            solve_host()
+        h1.record(stream)
+        h1.synchronize()
+        ems = h0.elapsed_time(h1)
+        nbytes = Fh.numel() * 8
+        e2e = {"value": world * K * esteps / (ems / 1e3), "unit": "RHS/s", "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "steps": esteps}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel (forward sweep) and of the whole solve
+    pk = measured_peaks()
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    fp64 = fp64_peak_tflops(torch)
+    nint = interior_rows(n, plan.nranges, plan.L)
+    fwd_flops = 6.0 * m * m * K * nint
+    fwd_bytes = 8.0 * (3 * m * m + 2 * m * K) * nint
+    tot_flops = 10.0 * m * m * K * n
+    tot_bytes = 8.0 * (5 * m * m + 4 * m * K) * n
+    hbm_bound = tot_flops / (fp64 * 1e12) < tot_bytes / (hbm * 1e9)
+    t_fwd = ph[0] / 1e3
+    if hbm_bound:
+        roof = {"bound": "hbm", "achieved": fwd_bytes / t_fwd / 1e9, "peak": hbm, "unit": "GB/s"}
+    else:
+        roof = {"bound": "tensor", "achieved": fwd_flops / t_fwd / 1e12, "peak": fp64, "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = ncu_traffic(name)
+    roof["kernel"] = "chain_fwd_kernel" if plan.mode == 0 else "gemm_batched_kernel (mode 1)"
+    roof["peak_source"] = ("cuBLAS DGEMM 4096^3 measured in this run (fp64 tensor)" if not hbm_bound
+                           else "MEASURED_PEAKS.json hbm_gbs")
+    t_roof = max(tot_flops / (fp64 * 1e12), tot_bytes / (hbm * 1e9))
+    clocks = clk.summary()
+
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        v, t, sample = cpu_sample_run(name)
+        cpu = {"value": v, "unit": "RHS/s", "cores": 1, "kind": "port", "sample": sample}
+
+    line = {
+        "metric": "rhs_columns_per_second", "value": value, "unit": "RHS/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded torch Philox on device; BASELINE.json distributions)",
+        "config": {"workload": name, "n": n, "m": m, "k": K, "ranks": bc["ranks"], "split": bc["split"],
+                   "device_ranges": plan.nranges, "L": plan.L, "mode": plan.mode,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (F %.2f GB, factors %.2f GB)" % (F.numel() * 8 / 1e9,
+                                                                                  plan.factor_bytes / 1e9)},
+        "roofline": roof,
+        "solve_roofline": {"flops": tot_flops, "bytes": tot_bytes, "t_roof_ms": t_roof * 1e3,
+                           "frac": t_roof * 1e3 / ms_step, "fp64_tflops_peak": fp64, "hbm_gbs_peak": hbm},
+        "phases_ms": {"forward": ph[0], "interface_tree": ph[1], "backward": ph[2], "total": ph[3]},
+        "plan_build_s": build_s,
+        "rel_residual": res,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "gpu_launches": launches,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def ncu_traffic(name):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get(name)
+    except (OSError, ValueError):
+        return None
+
+
+def residual_check(torch, name, X, F, configs):
+    """max|P X - F| / max|F| on the device (ref cli.py:211-214), matrix regenerated."""
+    diag, lower, upper, _ = configs.generate(name, device="cuda", k=0)
+    y = torch.bmm(diag, X)
+    y[1:] -= torch.bmm(lower, X[:-1])
+    y[:-1] -= torch.bmm(upper, X[1:])
+    r = ((y - F).abs().max() / F.abs().max()).item()
+    del diag, lower, upper, y
+    torch.cuda.empty_cache()
+    return r
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c1"), choices=sorted(BENCH_CFG))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--ranks", type=int, default=0)
+    ap.add_argument("--split", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-check", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -85,6 +85,13 @@ int btd_plan_solve_host(btd_plan* plan, const double* f_host, double* x_host, in
 int btd_plan_destroy(btd_plan* plan);
 int btd_plan_query(const btd_plan* plan, btd_plan_info* info);
 
+/* Per-phase device timing of solves (CUDA events recorded on the solve
+ * stream between the forward sweep, the interface/tree phase and the backward
+ * sweep).  ms_out[0..3] = forward, interface+tree, backward, total, summed
+ * over the solves since the last reset; *nsolves = how many. */
+int btd_plan_set_profiling(btd_plan* plan, int enable);
+int btd_plan_phase_times(btd_plan* plan, double* ms_out, int64_t* nsolves, int reset);
+
 /* Kernel launches issued by this library since load (the bench's
  * gpu_launches evidence) and the last error text. */
 int64_t btd_launch_count(void);

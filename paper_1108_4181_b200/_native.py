@@ -29,6 +29,8 @@ EXPORTS = (
     "btd_plan_solve_host",
     "btd_plan_destroy",
     "btd_plan_query",
+    "btd_plan_set_profiling",
+    "btd_plan_phase_times",
     "btd_launch_count",
     "btd_last_error",
     "btd_version",
@@ -69,6 +71,10 @@ def load():
     lib.btd_plan_destroy.restype = i32
     lib.btd_plan_query.argtypes = [vp, ctypes.POINTER(PlanInfo)]
     lib.btd_plan_query.restype = i32
+    lib.btd_plan_set_profiling.argtypes = [vp, i32]
+    lib.btd_plan_set_profiling.restype = i32
+    lib.btd_plan_phase_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64), i32]
+    lib.btd_plan_phase_times.restype = i32
     lib.btd_launch_count.argtypes = []
     lib.btd_launch_count.restype = i64
     lib.btd_last_error.argtypes = []

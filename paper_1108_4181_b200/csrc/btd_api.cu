@@ -253,6 +253,39 @@ struct btd_plan {
   int64_t hostio_k = 0;
   std::mutex mu;
   cudaStream_t last_stream = nullptr;
+  // profiling: 4 events per solve (before fwd, after fwd, after tree, after bwd)
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_free, ev_pending;
+  double phase_ms[4] = {0, 0, 0, 0};
+  int64_t nprof = 0;
+  cudaEvent_t ev_get() {
+    if (!ev_free.empty()) { cudaEvent_t e = ev_free.back(); ev_free.pop_back(); return e; }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+  void ev_mark(int slot, cudaStream_t st) {
+    if (!profiling) return;
+    cudaEvent_t e = ev_get();
+    CK(cudaEventRecord(e, st));
+    ev_pending.push_back(e);
+    (void)slot;
+  }
+  void ev_drain() {
+    for (size_t i = 0; i + 3 < ev_pending.size(); i += 4) {
+      float t[3];
+      CK(cudaEventSynchronize(ev_pending[i + 3]));
+      for (int p = 0; p < 3; ++p) CK(cudaEventElapsedTime(&t[p], ev_pending[i + p], ev_pending[i + p + 1]));
+      phase_ms[0] += t[0]; phase_ms[1] += t[1]; phase_ms[2] += t[2]; phase_ms[3] += t[0] + t[1] + t[2];
+      ++nprof;
+    }
+    for (auto e : ev_pending) ev_free.push_back(e);
+    ev_pending.clear();
+  }
+  ~btd_plan() {
+    for (auto e : ev_pending) cudaEventDestroy(e);
+    for (auto e : ev_free) cudaEventDestroy(e);
+  }
   int64_t factor_bytes = 0;
 
   template <class T>
@@ -796,6 +829,7 @@ void solve_device(btd_plan& pl, const double* F, double* X, int64_t K, cudaStrea
   double* base = pl.base.d();
   double* xt = pl.xt.d();
   double* z = pl.zbuf.d();
+  pl.ev_mark(0, st);
   if (pl.mode == 0) {
     ChainArgs a;
     a.lo = pl.d_lo; a.nint = pl.d_nint; a.slot0 = pl.d_slot0; a.nr = (int)nr;
@@ -822,6 +856,7 @@ void solve_device(btd_plan& pl, const double* F, double* X, int64_t K, cudaStrea
                   {term(mk(pool, pl.d_slot0, pl.off_Tb + j, blk, mp), mk(X, pl.d_lo, 1 + j, mK, K), m)}, st);
     }
   }
+  pl.ev_mark(1, st);
   // interface RHS (ref dichotomy.py:239-276): f~_q = base_q + Fc_{q-1} y_{q-1,last}
   launch_gemm(mp, K, pl.ncarry, mk(base, pl.carry_q, 0, mpK, K), mk(base, pl.carry_q, 0, mpK, K), 1.0,
               {term(mk(pool, pl.carry_fc, 0, blk, mp), mk(X, pl.carry_row, 0, mK, K), m)}, st);
@@ -839,6 +874,7 @@ void solve_device(btd_plan& pl, const double* F, double* X, int64_t K, cudaStrea
                  term(mk(pl.EH.d(), lev.h_idx, 0, blk, mp), mk(xt, lev.xh_idx, 0, mpK, K), mp)},
                 st);
   }
+  pl.ev_mark(2, st);
   if (pl.mode == 0) {
     ChainArgs a;
     a.lo = pl.d_lo; a.nint = pl.d_nint; a.slot0 = pl.d_slot0; a.nr = (int)nr;
@@ -864,6 +900,7 @@ void solve_device(btd_plan& pl, const double* F, double* X, int64_t K, cudaStrea
                   st);
     }
   }
+  pl.ev_mark(3, st);
 }
 
 }  // namespace
@@ -963,6 +1000,31 @@ int btd_plan_destroy(btd_plan* pl) {
     cudaDeviceSynchronize();
     delete pl;
     if (prev >= 0) cudaSetDevice(prev);
+  }
+  return BTD_OK;
+}
+
+int btd_plan_set_profiling(btd_plan* pl, int enable) {
+  if (!pl) return BTD_ERR_INVALID_ARG;
+  std::lock_guard<std::mutex> lk(pl->mu);
+  pl->profiling = enable != 0;
+  return BTD_OK;
+}
+
+int btd_plan_phase_times(btd_plan* pl, double* ms_out, int64_t* nsolves, int reset) {
+  if (!pl || !ms_out) return BTD_ERR_INVALID_ARG;
+  try {
+    DeviceGuard dg(pl->device);
+    std::lock_guard<std::mutex> lk(pl->mu);
+    pl->ev_drain();
+    for (int i = 0; i < 4; ++i) ms_out[i] = pl->phase_ms[i];
+    if (nsolves) *nsolves = pl->nprof;
+    if (reset) {
+      for (double& v : pl->phase_ms) v = 0;
+      pl->nprof = 0;
+    }
+  } catch (const BtdError& e) {
+    return e.code;
   }
   return BTD_OK;
 }
