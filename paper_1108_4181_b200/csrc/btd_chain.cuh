@@ -222,14 +222,86 @@ struct ChainCfg {
   static constexpr int RW = MP / WR, CW = KT / WC;
   static constexpr int TM = RW / 8, TN = CW / 8;
   static constexpr int LD = KT + 2;  // == 2 (mod 16) when KT % 16 == 0
-  static constexpr int PF = MP >= 128 ? 2 : (MP >= 32 ? 2 : 1);
+  static constexpr int NS = MP / 8;  // pair steps per block product
+  // factor-fragment prefetch distance (pair steps), one group ahead
+  static constexpr int PF = NS < 4 ? NS : (TM >= 4 ? 2 : 4);
+  static constexpr int GPS = NS / PF;  // groups per segment
   static_assert(RW % 8 == 0 && CW % 8 == 0, "warp tile must be a multiple of 8x8");
+  static_assert(NS % PF == 0, "prefetch groups must tile a segment");
 };
 
+// One prefetch group: PF pair steps of  acc += A_seg @ Bs, consuming the
+// register ring `buf` and refilling it with the next group's fragments
+// (`nxt` points at that group's first fragment; nullptr = stream end).
+template <int MP, int TM, int TN, int PF>
+BTD_DEVINL void group_mma(double (&acc)[TM][TN][2], double2 (&buf)[PF][TM], const double* __restrict__ nxt,
+                          const double* __restrict__ Bs, int ldb, int s0, int g, int t) {
+#pragma unroll
+  for (int u = 0; u < PF; ++u) {
+    double2 a[TM];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) a[i] = buf[u][i];
+    if (nxt) {
+#pragma unroll
+      for (int i = 0; i < TM; ++i) buf[u][i] = ldg_cg2(nxt + (i * 8 + g) * MP + 8 * u + 2 * t);
+    }
+    const int s = s0 + u;
+    double b0[TN], b1[TN];
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      b0[j] = Bs[(8 * s + 2 * t) * ldb + j * 8 + g];
+      b1[j] = Bs[(8 * s + 2 * t + 1) * ldb + j * 8 + g];
+    }
+    // all k-slot-0 products first, then k-slot-1: consecutive DMMAs are independent
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b0[j]);
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b1[j]);
+  }
+}
+
+template <int MP, int TM, int PF>
+BTD_DEVINL void group_load(double2 (&buf)[PF][TM], const double* __restrict__ p, int g, int t) {
+#pragma unroll
+  for (int u = 0; u < PF; ++u)
+#pragma unroll
+    for (int i = 0; i < TM; ++i) buf[u][i] = ldg_cg2(p + (i * 8 + g) * MP + 8 * u + 2 * t);
+}
+
+// Walks the factor-fragment stream (row j, segment, group) in execution order.
+template <int MP, int PF, int GPS, int NSEG>
+struct FragCursor {
+  const double* seg0;
+  const double* seg1;
+  const double* seg2;
+  int j, seg, grp, nrows;
+  BTD_DEVINL const double* ptr() const {
+    if (j >= nrows) return nullptr;
+    const double* b = seg == 0 ? seg0 : (seg == 1 ? seg1 : seg2);
+    return b + (int64_t)j * MP * MP + grp * 8 * PF;
+  }
+  BTD_DEVINL void advance() {
+    if (++grp == GPS) {
+      grp = 0;
+      if (++seg == NSEG) {
+        seg = 0;
+        ++j;
+      }
+    }
+  }
+};
+
+// Forward sweep.  Per interior row j, three segments stream through the same
+// register ring:  seg0 acc += AD_j y_{j-1};  seg1 ser += Tb_{j-1} y_{j-1};
+// seg2 acc += Dinv_j f_g.  (At j = 0, y_{-1} = 0 and seg1 reuses Tb_0.)
 template <int MP, int KT, int WR, int WC>
 __global__ void __launch_bounds__(32 * WR * WC) chain_fwd_kernel(ChainArgs a) {
   using Cfg = ChainCfg<MP, KT, WR, WC>;
-  constexpr int TM = Cfg::TM, TN = Cfg::TN, LD = Cfg::LD, NT = Cfg::NT, PF = Cfg::PF;
+  constexpr int TM = Cfg::TM, TN = Cfg::TN, LD = Cfg::LD, NT = Cfg::NT, PF = Cfg::PF, GPS = Cfg::GPS;
   extern __shared__ __align__(16) double sm[];
   double* Ys = sm;
   double* Fs0 = sm + MP * LD;
@@ -249,46 +321,69 @@ __global__ void __launch_bounds__(32 * WR * WC) chain_fwd_kernel(ChainArgs a) {
   const int nint = a.nint[q];
   const int64_t slot0 = a.slot0[q];
   const int64_t blk = (int64_t)MP * MP;
-  const int64_t rowK = (int64_t)a.m * K;  // elements per block row of F/X
+  const int64_t rowK = (int64_t)a.m * K;
 
   double ser[TM][TN][2];
   if (lo < a.n)
     load_tile(ser, a.F + lo * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
   else
     zero_acc(ser);
-
-  if (nint > 0) {
-    cp_tile<MP, KT, LD, NT>(Fs0, a.F + (lo + 1) * rowK, K, c0, a.m, vec);
-    cp_async_wait_all();
+  if (nint <= 0) {
+    store_tile(ser, a.base + (int64_t)q * MP * K, K, r0, c0 + cw0, MP, g, t, vec);
+    return;
   }
+  cp_tile<MP, KT, LD, NT>(Fs0, a.F + (lo + 1) * rowK, K, c0, a.m, vec);
+
+  FragCursor<MP, PF, GPS, 3> cur;
+  cur.seg0 = a.AD + slot0 * blk + r0 * MP;
+  cur.seg1 = a.Tb + slot0 * blk + r0 * MP;  // row j uses Tb_{j-1}: offset below
+  cur.seg2 = a.Dinv + slot0 * blk + r0 * MP;
+  cur.j = 0; cur.seg = 0; cur.grp = 0; cur.nrows = nint;
+  // Tb_{j-1}: shift seg1 by one block, except row 0 which reuses Tb_0 (times y_{-1} = 0)
+  double2 buf[PF][TM];
+  group_load<MP, TM, PF>(buf, cur.ptr(), g, t);
+  cp_async_wait_all();
   __syncthreads();
+
+  double acc[TM][TN][2];
+  zero_acc(acc);
   for (int j = 0; j < nint; ++j) {
     const int64_t gr = lo + 1 + j;
-    double* Fcur = (j & 1) ? Fs1 : Fs0;
+    const double* Fcur = (j & 1) ? Fs1 : Fs0;
     double* Fnxt = (j & 1) ? Fs0 : Fs1;
     if (j + 1 < nint) cp_tile<MP, KT, LD, NT>(Fnxt, a.F + (gr + 1) * rowK, K, c0, a.m, vec);
-    double acc[TM][TN][2];
-    zero_acc(acc);
-    const int64_t sl = slot0 + j;
-    wgemm<MP, TM, TN, PF>(acc, a.Dinv + sl * blk + r0 * MP, Fcur + cw0, LD, g, t);
-    if (j > 0)
-      wgemm2<MP, TM, TN, PF>(acc, a.AD + sl * blk + r0 * MP, ser, a.Tb + (sl - 1) * blk + r0 * MP,
-                             Ys + cw0, LD, g, t);
+#pragma unroll 1
+    for (int seg = 0; seg < 3; ++seg) {
+#pragma unroll 1
+      for (int grp = 0; grp < GPS; ++grp) {
+        cur.advance();
+        const double* nx = cur.ptr();
+        if (nx && cur.seg == 1 && cur.j > 0) nx -= blk;  // Tb_{j-1}
+        if (seg == 0)
+          group_mma<MP, TM, TN, PF>(acc, buf, nx, Ys + cw0, LD, grp * PF, g, t);
+        else if (seg == 1)
+          group_mma<MP, TM, TN, PF>(ser, buf, nx, Ys + cw0, LD, grp * PF, g, t);
+        else
+          group_mma<MP, TM, TN, PF>(acc, buf, nx, Fcur + cw0, LD, grp * PF, g, t);
+      }
+    }
     __syncthreads();
     store_smem(acc, Ys, LD, r0, cw0, g, t);
     store_tile(acc, a.X + gr * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
+    zero_acc(acc);
     cp_async_wait_all();
     __syncthreads();
   }
-  if (nint > 0)
-    wgemm<MP, TM, TN, PF>(ser, a.Tb + (slot0 + nint - 1) * blk + r0 * MP, Ys + cw0, LD, g, t);
+  wgemm<MP, TM, TN, 2>(ser, a.Tb + (slot0 + nint - 1) * blk + r0 * MP, Ys + cw0, LD, g, t);
   store_tile(ser, a.base + (int64_t)q * MP * K, K, r0, c0 + cw0, MP, g, t, vec);
 }
 
+// Backward sweep: per row j (descending) two segments through one ring:
+// seg0 acc += G_j x~_q ; seg1 acc += S_j x_{j+1}, with acc initialised to y_j.
 template <int MP, int KT, int WR, int WC>
 __global__ void __launch_bounds__(32 * WR * WC) chain_bwd_kernel(ChainArgs a) {
   using Cfg = ChainCfg<MP, KT, WR, WC>;
-  constexpr int TM = Cfg::TM, TN = Cfg::TN, LD = Cfg::LD, NT = Cfg::NT, PF = Cfg::PF;
+  constexpr int TM = Cfg::TM, TN = Cfg::TN, LD = Cfg::LD, NT = Cfg::NT, PF = Cfg::PF, GPS = Cfg::GPS;
   extern __shared__ __align__(16) double sm[];
   double* Xq = sm;
   double* Xn = sm + MP * LD;
@@ -312,26 +407,49 @@ __global__ void __launch_bounds__(32 * WR * WC) chain_bwd_kernel(ChainArgs a) {
 
   cp_tile<MP, KT, LD, NT>(Xq, a.xt + (int64_t)q * xtK, K, c0, MP, vec);
   cp_tile<MP, KT, LD, NT>(Xn, a.xt + (int64_t)(q + 1) * xtK, K, c0, MP, vec);
-  double y[TM][TN][2];
-  if (nint > 0) load_tile(y, a.X + (lo + nint) * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
   if (lo < a.n) {  // x[lo] = x~_q  (ref dichotomy.py:351)
     double xq[TM][TN][2];
     load_tile(xq, a.xt + (int64_t)q * xtK, K, r0, c0 + cw0, MP, g, t, vec);
     store_tile(xq, a.X + lo * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
   }
+  if (nint <= 0) {
+    cp_async_wait_all();
+    return;
+  }
+  // rows run j = nint-1 .. 0: the stream walks slots downward
+  FragCursor<MP, PF, GPS, 2> cur;
+  cur.seg0 = a.G + (slot0 + nint - 1) * blk + r0 * MP;
+  cur.seg1 = a.S + (slot0 + nint - 1) * blk + r0 * MP;
+  cur.seg2 = nullptr;
+  cur.j = 0; cur.seg = 0; cur.grp = 0; cur.nrows = nint;
+  double2 buf[PF][TM];
+  {
+    const double* p0 = cur.ptr();
+    group_load<MP, TM, PF>(buf, p0, g, t);
+  }
+  double y[TM][TN][2];
+  load_tile(y, a.X + (lo + nint) * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
   cp_async_wait_all();
   __syncthreads();
-  for (int j = nint - 1; j >= 0; --j) {
+  for (int jj = 0; jj < nint; ++jj) {
+    const int j = nint - 1 - jj;
     const int64_t gr = lo + 1 + j;
     double acc[TM][TN][2];
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
-      for (int jj = 0; jj < TN; ++jj) { acc[i][jj][0] = y[i][jj][0]; acc[i][jj][1] = y[i][jj][1]; }
+      for (int c = 0; c < TN; ++c) { acc[i][c][0] = y[i][c][0]; acc[i][c][1] = y[i][c][1]; }
     if (j > 0) load_tile(y, a.X + (gr - 1) * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
-    const int64_t sl = slot0 + j;
-    wgemm<MP, TM, TN, PF>(acc, a.G + sl * blk + r0 * MP, Xq + cw0, LD, g, t);
-    wgemm<MP, TM, TN, PF>(acc, a.S + sl * blk + r0 * MP, Xn + cw0, LD, g, t);
+#pragma unroll 1
+    for (int seg = 0; seg < 2; ++seg) {
+#pragma unroll 1
+      for (int grp = 0; grp < GPS; ++grp) {
+        cur.advance();
+        const double* nx = cur.ptr();
+        if (nx) nx -= 2 * (int64_t)cur.j * blk;  // cursor rows advance upward; slots go down
+        group_mma<MP, TM, TN, PF>(acc, buf, nx, (seg == 0 ? Xq : Xn) + cw0, LD, grp * PF, g, t);
+      }
+    }
     __syncthreads();
     store_smem(acc, Xn, LD, r0, cw0, g, t);
     store_tile(acc, a.X + gr * rowK, K, r0, c0 + cw0, a.m, g, t, vec);

@@ -134,10 +134,11 @@ __global__ void __launch_bounds__(128) gemm_batched_kernel(GemmDesc d) {
 #pragma unroll
           for (int i = 0; i < TM; ++i)
 #pragma unroll
-            for (int j = 0; j < TN; ++j) {
-              dmma(acc[i][j][0], acc[i][j][1], a[i].x, b0[j]);
-              dmma(acc[i][j][0], acc[i][j][1], a[i].y, b1[j]);
-            }
+            for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b0[j]);
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b1[j]);
         }
       }
       __syncthreads();
