@@ -41,20 +41,34 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# Per-config plan parameters.  ranks = the reference's P; split = on-device
-# second-level ranges per reference range (hard part 1).
+# Per-config plan parameters.  ranks = the reference's P (subdomains);
+# split = on-device second-level ranges per subdomain (hard
+# part 1), chosen so each GPU runs ~`ranges_per_gpu` device ranges (one CTA
+# per range and column tile fills the 148 SMs).  c4 follows the paired
+# reading of BASELINE.json: 8 / 16 / 32 / 64 subdomains per GPU on 1 / 2 / 4 / 8 GPUs.
 BENCH_CFG = {
-    "c0": dict(ranks=4, split=1, dtype="f64"),
-    "c1": dict(ranks=18, split=1, dtype="f64"),
-    "c2": dict(ranks=9, split=1, dtype="f64"),
-    "c4": dict(ranks=8, split=74, dtype="f64"),
+    "c0": dict(subdomains_per_gpu=lambda w: 4, ranges_per_gpu=4),
+    "c1": dict(subdomains_per_gpu=lambda w: 18, ranges_per_gpu=18),
+    "c2": dict(subdomains_per_gpu=lambda w: 9, ranges_per_gpu=9),
+    "c4": dict(subdomains_per_gpu=lambda w: 8 * w, ranges_per_gpu=592),
 }
-# CPU sample per config: (block rows, columns, ranks) of the same operator family
+
+
+def plan_params(name, world, ranks=0, split=0):
+    bc = BENCH_CFG[name]
+    spg = bc["subdomains_per_gpu"](world)
+    r = ranks or spg * world
+    sp = split or max(1, -(-bc["ranges_per_gpu"] // spg))
+    return r, sp
+
+
+# CPU sample per config: (block rows, columns, ranks) of the same operator family,
+# sized for a few seconds of host work per step.
 CPU_SAMPLE = {
     "c0": (512, 32, 4),
-    "c1": (64, 16, 2),
-    "c2": (256, 64, 4),
-    "c4": (8192, 8, 8),
+    "c1": (256, 256, 8),
+    "c2": (512, 1024, 8),
+    "c4": (65536, 64, 16),
 }
 
 
@@ -160,36 +174,50 @@ def interior_rows(n, nranges, L):
 
 
 # --------------------------------------------------------------------------- CPU arm
-def cpu_sample_run(name, steps=1, warmup=0):
-    """Time the oracle port of the reference plan_solve on a bounded sample of
-    config `name`; returns (rhs_per_s scaled to full size, seconds, sample text)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import blocktri_oracle as O
-    from paper_1108_4181_b200 import configs
+class CpuSample:
+    """The reference algorithm on the host (oracle/liboracle.so: C port of the
+    reference's compiled path, ranges and column chunks on all host threads)
+    over a bounded sample of config `name`; plan built once (untimed)."""
 
-    cfg = configs.CONFIGS[name]
-    ns, ks, ps = CPU_SAMPLE[name]
-    if cfg["kind"] == "strip":
-        d, lo, up, f = configs.strip_numpy(ns, cfg["m"], ks, cfg["shift"], 0)
-    else:
-        d, lo, up, f = configs.dominant_numpy(ns, cfg["m"], ks, 0)
-    plan = O.plan_build(d, lo, up, ps)
-    for _ in range(warmup):
-        O.plan_solve(plan, f)
-    ts = []
-    for _ in range(max(1, steps)):
+    def __init__(self, name):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import coracle
+        from paper_1108_4181_b200 import configs
+
+        self.coracle = coracle
+        cfg = configs.CONFIGS[name]
+        self.cfg = cfg
+        ns, ks, ps = CPU_SAMPLE[name]
+        if cfg["kind"] == "strip":
+            d, lo, up, f = configs.strip_numpy(ns, cfg["m"], ks, cfg["shift"], 0)
+        else:
+            d, lo, up, f = configs.dominant_numpy(ns, cfg["m"], ks, 0)
+        self.f = f
+        self.ns, self.ks, self.ps = ns, ks, ps
+        self.plan = coracle.CPlan(d, lo, up, ps)
+        self.cores = coracle.threads()
+        self.sample = (f"C port of the reference plan_solve (oracle/blocktri_oracle.c; ref dichotomy.py:358-390, "
+                       f"_kernels.pyx:173-194) on N={ns} of {cfg['n']} block rows, K={ks} of {cfg['k']} columns, "
+                       f"P={ps}, {self.cores} threads; RHS/s scaled by N_s/N (solve cost is linear in N)")
+
+    def step(self):
         t0 = time.perf_counter()
-        O.plan_solve(plan, f)
-        ts.append(time.perf_counter() - t0)
-    t = statistics.median(ts)
-    # plan_solve is linear in N*K at fixed M: full-size RHS/s = K_s/t * N_s/N
-    value = ks / t * ns / cfg["n"]
-    sample = (f"oracle port (numpy, ref dichotomy.py:358-390) on N={ns} of {cfg['n']} block rows, "
-              f"K={ks} of {cfg['k']} columns, P={ps}; RHS/s scaled by N_s/N")
-    return value, t, sample
+        self.plan.solve(self.f)
+        t = time.perf_counter() - t0
+        return self.ks / t * self.ns / self.cfg["n"], t
+
+
+def cpu_sample_run(name, steps=1):
+    cs = CpuSample(name)
+    vals = [cs.step() for _ in range(max(1, steps))]
+    v = statistics.median(x[0] for x in vals)
+    t = statistics.median(x[1] for x in vals)
+    return v, t, cs.sample, cs.cores, "port"
 
 
 def run_reference(args):
+    """--impl reference: the reference's CPU algorithm on this host's cores
+    (rank 0 only; other ranks exit without work)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -197,28 +225,19 @@ def run_reference(args):
     from paper_1108_4181_b200 import configs
 
     cfg = configs.CONFIGS[name]
-    ts = []
-    vals = []
-    for i in range(args.warmup + args.steps):
-        v, t, sample = cpu_sample_run(name)
-        if i >= args.warmup:
-            ts.append(t)
-            vals.append(v)
-    value = statistics.median(vals)
-    cores = 1
-    try:
-        import threadpoolctl
-
-        cores = max(1, max((p.get("num_threads", 1) for p in threadpoolctl.threadpool_info()), default=1))
-    except Exception:
-        pass
+    cs = CpuSample(name)
+    for _ in range(args.warmup):
+        cs.step()
+    res = [cs.step() for _ in range(args.steps)]
+    ts = [r[1] for r in res]
+    value = cs.ks * args.steps / sum(ts) * cs.ns / cfg["n"]
     line = {
         "impl": "reference", "metric": "rhs_columns_per_second", "value": value, "unit": "RHS/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * statistics.median(ts), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * sum(ts) / len(ts), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy, BASELINE.json distributions)",
-        "config": {"workload": name, "n": cfg["n"], "m": cfg["m"], "k": cfg["k"], "ranks": CPU_SAMPLE[name][2]},
-        "cpu_baseline": {"value": value, "unit": "RHS/s", "cores": cores, "kind": "port", "sample": sample},
+        "config": {"workload": name, "n": cfg["n"], "m": cfg["m"], "k": cfg["k"], "sample_ranks": cs.ps},
+        "cpu_baseline": {"value": value, "unit": "RHS/s", "cores": cs.cores, "kind": "port", "sample": cs.sample},
         "e2e": {"value": value, "unit": "RHS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -226,6 +245,8 @@ def run_reference(args):
 
 # --------------------------------------------------------------------------- GPU arm
 def run_b200(args):
+    import ctypes
+
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -233,98 +254,116 @@ def run_b200(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
     from paper_1108_4181_b200 import _native, configs, plan_build_arrays
+    from paper_1108_4181_b200.distributed import ShardedPlan
 
     name = args.config
     cfg = configs.CONFIGS[name]
-    bc = dict(BENCH_CFG[name])
-    if args.ranks:
-        bc["ranks"] = args.ranks
-    if args.split:
-        bc["split"] = args.split
+    ranks, split = plan_params(name, world, args.ranks, args.split)
     n, m, K = cfg["n"], cfg["m"], cfg["k"]
     lib = _native.load()
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
 
+    # every rank draws the same global matrix / RHS (seeded, on device) and keeps its rows
     diag, lower, upper, F = make_inputs(name, torch)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    plan = plan_build_arrays(diag, lower, upper, bc["ranks"], split=bc["split"])
+    if not sharded:
+        plan = plan_build_arrays(diag, lower, upper, ranks, split=split)
+        row_lo, row_hi = 0, n
+        nranges, L, mode, fbytes = plan.nranges, plan.L, plan.mode, plan.factor_bytes
+        handle = plan.handle
+    else:
+        plan = ShardedPlan(diag, lower, upper, ranks, split=split)
+        row_lo, row_hi = plan.row_lo, plan.row_hi
+        F = F[row_lo:row_hi].contiguous()
+        info = plan.be.info(plan.h)
+        nranges, L, mode, fbytes = plan.nranges, plan.L, int(info.mode), int(info.factor_bytes)
+        handle = plan.h
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     del diag, lower, upper
     torch.cuda.empty_cache()
     X = torch.empty_like(F)
-    stream = torch.cuda.current_stream()
-    sp = __import__("ctypes").c_void_p(stream.cuda_stream)
 
-    def solve():
-        st = lib.btd_plan_solve(plan.handle, __import__("ctypes").c_void_p(F.data_ptr()),
-                                __import__("ctypes").c_void_p(X.data_ptr()), K, sp)
-        if st:
-            _native.check(st)
+    if not sharded:
+        def solve():
+            st = lib.btd_plan_solve(handle, ctypes.c_void_p(F.data_ptr()), ctypes.c_void_p(X.data_ptr()), K, sp)
+            if st:
+                _native.check(st)
+    else:
+        def solve():
+            plan.solve(F, out=X)
 
-    for _ in range(args.warmup):
-        solve()
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    lc0 = _native.launch_count()
     with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            solve()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        lc0 = _native.launch_count()
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(args.steps):
             solve()
         e1.record(stream)
         e1.synchronize()
-    launches = _native.launch_count() - lc0
+        launches = _native.launch_count() - lc0
+        if dist:
+            dist.barrier()
     ms = e0.elapsed_time(e1)
     if dist:
         tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     ms_step = ms / args.steps
-    value = world * K * args.steps / (ms / 1e3)
+    value = K * args.steps / (ms / 1e3)  # whole job: K columns per step over all GPUs
 
-    # per-phase timing (separate profiled pass: events between the phases)
-    lib.btd_plan_set_profiling(plan.handle, 1)
-    import ctypes
-
+    # per-phase device timing (separate profiled pass; events between the phases)
     buf = (ctypes.c_double * 4)()
     nsv = ctypes.c_int64()
-    lib.btd_plan_phase_times(plan.handle, buf, ctypes.byref(nsv), 1)
+    lib.btd_plan_set_profiling(handle, 1)
+    lib.btd_plan_phase_times(handle, buf, ctypes.byref(nsv), 1)
     for _ in range(args.steps):
         solve()
     torch.cuda.synchronize()
-    lib.btd_plan_phase_times(plan.handle, buf, ctypes.byref(nsv), 1)
-    lib.btd_plan_set_profiling(plan.handle, 0)
+    lib.btd_plan_phase_times(handle, buf, ctypes.byref(nsv), 1)
+    lib.btd_plan_set_profiling(handle, 0)
     ph = [buf[i] / max(1, nsv.value) for i in range(4)]
 
-    # correctness spot check at full size: relative residual of one solve
     res = None
-    if not args.no_check:
+    if not args.no_check and not sharded:
         res = residual_check(torch, name, X, F, configs)
 
-    # e2e through the host API with pinned host buffers
+    # e2e through the host-memory API: pinned host F -> device -> solve -> host X
     e2e = None
     if not args.no_e2e:
         Fh = F.cpu().pin_memory()
         Xh = torch.empty_like(Fh).pin_memory()
-        del X
-        torch.cuda.empty_cache()
-
-        def solve_host():
-            st = lib.btd_plan_solve_host(plan.handle, ctypes.c_void_p(Fh.data_ptr()), ctypes.c_void_p(Xh.data_ptr()),
-                                         K, sp)
-            if st:
-                _native.check(st)
-
+        if not sharded:
+            def solve_host():
+                st = lib.btd_plan_solve_host(handle, ctypes.c_void_p(Fh.data_ptr()), ctypes.c_void_p(Xh.data_ptr()),
+                                             K, sp)
+                if st:
+                    _native.check(st)
+        else:
+            def solve_host():
+                F.copy_(Fh, non_blocking=True)
+                Xh.copy_(plan.solve(F, out=X), non_blocking=True)
+                torch.cuda.current_stream().synchronize()
         solve_host()
         torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
         h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         esteps = max(1, min(args.steps, 5))
         h0.record(stream)
@@ -333,8 +372,12 @@ def run_b200(args):
         h1.record(stream)
         h1.synchronize()
         ems = h0.elapsed_time(h1)
+        if dist:
+            tt = torch.tensor([ems], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
         nbytes = Fh.numel() * 8
-        e2e = {"value": world * K * esteps / (ems / 1e3), "unit": "RHS/s", "h2d_bytes_per_step": nbytes,
+        e2e = {"value": K * esteps / (ems / 1e3), "unit": "RHS/s", "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes, "steps": esteps}
 
     if rank != 0:
@@ -342,15 +385,15 @@ def run_b200(args):
             dist.destroy_process_group()
         return
 
-    # roofline of the dominant kernel (forward sweep) and of the whole solve
+    # roofline of the dominant kernel (forward sweep) and of the whole solve, per GPU
     pk = measured_peaks()
     hbm = float(pk.get("hbm_gbs", 6650.0))
     fp64 = fp64_peak_tflops(torch)
-    nint = interior_rows(n, plan.nranges, plan.L)
+    nint = interior_rows(n, nranges, L) / world
     fwd_flops = 6.0 * m * m * K * nint
     fwd_bytes = 8.0 * (3 * m * m + 2 * m * K) * nint
-    tot_flops = 10.0 * m * m * K * n
-    tot_bytes = 8.0 * (5 * m * m + 4 * m * K) * n
+    tot_flops = 10.0 * m * m * K * n / world
+    tot_bytes = 8.0 * (5 * m * m + 4 * m * K) * n / world
     hbm_bound = tot_flops / (fp64 * 1e12) < tot_bytes / (hbm * 1e9)
     t_fwd = ph[0] / 1e3
     if hbm_bound:
@@ -359,29 +402,31 @@ def run_b200(args):
         roof = {"bound": "tensor", "achieved": fwd_flops / t_fwd / 1e12, "peak": fp64, "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = ncu_traffic(name)
-    roof["kernel"] = "chain_fwd_kernel" if plan.mode == 0 else "gemm_batched_kernel (mode 1)"
-    roof["peak_source"] = ("cuBLAS DGEMM 4096^3 measured in this run (fp64 tensor)" if not hbm_bound
-                           else "MEASURED_PEAKS.json hbm_gbs")
+    roof["kernel"] = "chain_fwd_kernel" if mode == 0 else "gemm_batched_kernel (mode 1)"
+    roof["peak_source"] = ("cuBLAS DGEMM 4096^3 measured in this run (fp64 tensor; MEASURED_PEAKS.json has no fp64)"
+                           if not hbm_bound else "MEASURED_PEAKS.json hbm_gbs")
     t_roof = max(tot_flops / (fp64 * 1e12), tot_bytes / (hbm * 1e9))
     clocks = clk.summary()
 
     cpu = None
     if world == 1 and not args.no_cpu:
-        v, t, sample = cpu_sample_run(name)
-        cpu = {"value": v, "unit": "RHS/s", "cores": 1, "kind": "port", "sample": sample}
+        v, t, sample, cores, kind = cpu_sample_run(name)
+        cpu = {"value": v, "unit": "RHS/s", "cores": cores, "kind": kind, "sample": sample}
 
     line = {
         "metric": "rhs_columns_per_second", "value": value, "unit": "RHS/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if name in ("c0", "c1", "c2") else "weak-subdomains",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded torch Philox on device; BASELINE.json distributions)",
-        "config": {"workload": name, "n": n, "m": m, "k": K, "ranks": bc["ranks"], "split": bc["split"],
-                   "device_ranges": plan.nranges, "L": plan.L, "mode": plan.mode,
-                   "parallelism": "replicas" if world > 1 else "single",
-                   "l2": "inputs larger than L2 (F %.2f GB, factors %.2f GB)" % (F.numel() * 8 / 1e9,
-                                                                                  plan.factor_bytes / 1e9)},
+        "config": {"workload": name, "n": n, "m": m, "k": K, "ranks": ranks, "split": split,
+                   "device_ranges": nranges, "L": L, "mode": mode,
+                   "parallelism": f"rows sharded over {world} GPUs (NCCL all-gather of interface pairs)"
+                   if sharded else "single GPU",
+                   "l2": "inputs larger than L2 (F %.2f GB, factors %.2f GB per GPU)" % (
+                       F.numel() * 8 / 1e9, fbytes / 1e9)},
         "roofline": roof,
-        "solve_roofline": {"flops": tot_flops, "bytes": tot_bytes, "t_roof_ms": t_roof * 1e3,
+        "solve_roofline": {"flops_per_gpu": tot_flops, "bytes_per_gpu": tot_bytes, "t_roof_ms": t_roof * 1e3,
                            "frac": t_roof * 1e3 / ms_step, "fp64_tflops_peak": fp64, "hbm_gbs_peak": hbm},
         "phases_ms": {"forward": ph[0], "interface_tree": ph[1], "backward": ph[2], "total": ph[3]},
         "plan_build_s": build_s,
@@ -430,6 +475,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="use the row-sharded NCCL path even on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -58,6 +58,8 @@ typedef struct btd_plan_info {
   int64_t row_lo, row_hi;    /* block rows owned by this plan (sharded plans) */
   int32_t device;
   int32_t mode;              /* 0 = fused chain kernels, 1 = per-step GEMM sweep (large m) */
+  int32_t rank, world;       /* shard of a row-sharded plan (0, 1 when not sharded) */
+  int64_t range_lo, range_hi;/* device ranges owned by this shard */
 } btd_plan_info;
 
 /* Algorithm 2 step 1 (ref dichotomy.py:318-338): validate 1 <= ranks <= n
@@ -83,6 +85,35 @@ int btd_plan_solve_host(btd_plan* plan, const double* f_host, double* x_host, in
                         void* stream);
 
 int btd_plan_destroy(btd_plan* plan);
+
+/* ---- row-sharded (multi-GPU) plans and solves --------------------------
+ * The ranges (ranks*split of them, a multiple of `world`) are split
+ * contiguously over `world` processes, one GPU each; rank r owns ranges
+ * [r*P/world, (r+1)*P/world) and their block rows.  The reference's
+ * distributed solve (harness.py:147-216: local sweep, allgather of the
+ * (base, carry) interface pairs, reduced solve, local recovery) maps to:
+ *   plan:  btd_plan_create_shard (local factors + this shard's four
+ *          reduced-system contributions per range) -> caller all-gathers the
+ *          contributions (btd_shard_contrib) over NCCL -> btd_shard_finish
+ *          (reduced system + partition tree, identical on every rank);
+ *   solve: btd_shard_solve_a (local sweeps; writes this shard's (base, carry)
+ *          pairs, btd_shard_exchange_size doubles) -> caller all-gathers them
+ *          -> btd_shard_solve_b (interface RHS, tree, local recovery).
+ * f_local / x_local hold the shard's rows [row_lo, row_hi) (btd_plan_query).
+ * err_info[0] = SingularPivot row, err_info[1] = failing global range. */
+int btd_plan_create_shard(const double* diag, const double* lower, const double* upper,
+                          int64_t n, int64_t m, int64_t ranks, int64_t split, int rank, int world,
+                          int device, int flags, void* stream, btd_plan** out_plan,
+                          int64_t* err_info);
+/* copies this shard's contributions ([ranges][4][mp][mp] doubles) to device
+ * buffer dst (dst == NULL: only report *nelems) */
+int btd_shard_contrib(btd_plan* plan, double* dst, int64_t* nelems, void* stream);
+int btd_shard_finish(btd_plan* plan, const double* contrib_all, void* stream, int64_t* err_row);
+int btd_shard_exchange_size(const btd_plan* plan, int64_t k, int64_t* nelems_local);
+int btd_shard_solve_a(btd_plan* plan, const double* f_local, double* x_local, int64_t k,
+                      double* exch_local, void* stream);
+int btd_shard_solve_b(btd_plan* plan, const double* exch_all, const double* f_local,
+                      double* x_local, int64_t k, void* stream);
 int btd_plan_query(const btd_plan* plan, btd_plan_info* info);
 
 /* Per-phase device timing of solves (CUDA events recorded on the solve

@@ -29,6 +29,12 @@ EXPORTS = (
     "btd_plan_solve_host",
     "btd_plan_destroy",
     "btd_plan_query",
+    "btd_plan_create_shard",
+    "btd_shard_contrib",
+    "btd_shard_finish",
+    "btd_shard_exchange_size",
+    "btd_shard_solve_a",
+    "btd_shard_solve_b",
     "btd_plan_set_profiling",
     "btd_plan_phase_times",
     "btd_launch_count",
@@ -44,6 +50,8 @@ class PlanInfo(ctypes.Structure):
         ("L", ctypes.c_int64), ("tree_nodes", ctypes.c_int64), ("tree_depth", ctypes.c_int64),
         ("factor_bytes", ctypes.c_int64), ("row_lo", ctypes.c_int64), ("row_hi", ctypes.c_int64),
         ("device", ctypes.c_int32), ("mode", ctypes.c_int32),
+        ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+        ("range_lo", ctypes.c_int64), ("range_hi", ctypes.c_int64),
     ]
 
 
@@ -71,6 +79,19 @@ def load():
     lib.btd_plan_destroy.restype = i32
     lib.btd_plan_query.argtypes = [vp, ctypes.POINTER(PlanInfo)]
     lib.btd_plan_query.restype = i32
+    lib.btd_plan_create_shard.argtypes = [dp, dp, dp, i64, i64, i64, i64, i32, i32, i32, i32, vp,
+                                          ctypes.POINTER(vp), ctypes.POINTER(i64)]
+    lib.btd_plan_create_shard.restype = i32
+    lib.btd_shard_contrib.argtypes = [vp, dp, ctypes.POINTER(i64), vp]
+    lib.btd_shard_contrib.restype = i32
+    lib.btd_shard_finish.argtypes = [vp, dp, vp, ctypes.POINTER(i64)]
+    lib.btd_shard_finish.restype = i32
+    lib.btd_shard_exchange_size.argtypes = [vp, i64, ctypes.POINTER(i64)]
+    lib.btd_shard_exchange_size.restype = i32
+    lib.btd_shard_solve_a.argtypes = [vp, dp, dp, i64, dp, vp]
+    lib.btd_shard_solve_a.restype = i32
+    lib.btd_shard_solve_b.argtypes = [vp, dp, dp, dp, i64, vp]
+    lib.btd_shard_solve_b.restype = i32
     lib.btd_plan_set_profiling.argtypes = [vp, i32]
     lib.btd_plan_set_profiling.restype = i32
     lib.btd_plan_phase_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64), i32]

@@ -28,6 +28,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -211,48 +212,56 @@ std::vector<Node> partition_tree(int64_t count, int64_t* depth) {
 struct btd_plan {
   int device = 0;
   int64_t n = 0, m = 0, mp = 0, ranks = 0, split = 1, nr = 0, L = 0, npad = 0, cap = 0;
+  int rank = 0, world = 1;
+  int64_t q0 = 0, q1 = 0, nrl = 0;  // owned device ranges [q0, q1)
+  int64_t R0 = 0, nl = 0, nloc = 0;  // first owned (padded) row, owned padded rows, owned true rows
   int mode = 0;
   int64_t blk = 0;
-  std::vector<int64_t> lo, slot0;
-  std::vector<int32_t> nint;  // interior rows inside [0, n)
+  bool finished = false;
+  std::vector<int64_t> lo, slot0;  // per LOCAL range: interface row relative to R0, first factor slot
+  std::vector<int32_t> nint;       // per LOCAL range: interior rows inside [0, n)
   std::vector<std::unique_ptr<DevBuf>> arrays;
   const int64_t* d_lo = nullptr;
   const int64_t* d_slot0 = nullptr;
   const int32_t* d_nint = nullptr;
-  DevBuf pool;
+  DevBuf pool;     // local factor blocks + global reduced blocks
+  DevBuf contrib;  // [nrl][4][mp][mp]: C_lo - B_lo U[1],  A V_last,  A U_last,  B_lo V[1]
   int64_t off_AD = 0, off_Dinv = 0, off_S = 0, off_G = 0, off_Tb = 0, off_Fc = 0, off_Bif = 0,
           off_BU = 0, off_BV = 0, off_Dt = 0, off_Rd = 0, off_Rl = 0, off_Ru = 0, off_RdT = 0,
           off_RlT = 0, off_RuT = 0, off_Z = 0, off_I = 0;
-  // tree
+  // tree (global, identical on every rank)
   std::vector<Node> nodes;
   int64_t depth = 0;
   DevBuf Rrows, EH;
   const int64_t *d_roff = nullptr, *d_rld = nullptr, *d_nlo = nullptr;
+  // nodes this rank needs (its own interfaces + dependency closure), z batch over them
+  int nz = 0;
+  const int64_t *z_id = nullptr, *z_roff = nullptr, *z_rld = nullptr, *z_nlo = nullptr;
   struct Level {
     int count = 0;
     const int64_t *c_idx = nullptr, *z_idx = nullptr, *e_idx = nullptr, *xl_idx = nullptr,
                   *h_idx = nullptr, *xh_idx = nullptr;
   };
   std::vector<Level> levels;
-  // interface-RHS carry batch
+  // interface-RHS carry (local ranges whose last interior row exists)
   int ncarry = 0;
-  const int64_t *carry_q = nullptr, *carry_fc = nullptr, *carry_row = nullptr;
-  // mode-1 per-step batches
+  const int64_t *carry_src = nullptr, *carry_fc = nullptr, *carry_row = nullptr;
+  // mode-1 per-step batches (local ranges)
   struct Step1 {
-    int cnt = 0;          // ranges active at this step (prefix)
-    int nx = 0, nt = 0;   // bwd: entries whose next row is interior / is x~_{q+1}
+    int cnt = 0;
+    int nx = 0, nt = 0;
     const int64_t *x_row = nullptr, *x_slot = nullptr, *x_q = nullptr;
     const int64_t *t_row = nullptr, *t_slot = nullptr, *t_q = nullptr;
   };
   std::vector<Step1> steps1;
-  const int64_t* d_qiota = nullptr;
-  int nlive = 0;  // ranges whose interface row is < n
+  int nlive = 0;  // local ranges whose interface row is < n
   // scratch
   int64_t scratch_k = 0;
-  DevBuf base, zbuf, xt, hostio;
+  DevBuf ft, zbuf, xt, hostio;
   int64_t hostio_k = 0;
   std::mutex mu;
   cudaStream_t last_stream = nullptr;
+  int64_t factor_bytes = 0;
   // profiling: 4 events per solve (before fwd, after fwd, after tree, after bwd)
   bool profiling = false;
   std::vector<cudaEvent_t> ev_free, ev_pending;
@@ -264,12 +273,11 @@ struct btd_plan {
     CK(cudaEventCreate(&e));
     return e;
   }
-  void ev_mark(int slot, cudaStream_t st) {
+  void ev_mark(cudaStream_t st) {
     if (!profiling) return;
     cudaEvent_t e = ev_get();
     CK(cudaEventRecord(e, st));
     ev_pending.push_back(e);
-    (void)slot;
   }
   void ev_drain() {
     for (size_t i = 0; i + 3 < ev_pending.size(); i += 4) {
@@ -286,8 +294,6 @@ struct btd_plan {
     for (auto e : ev_pending) cudaEventDestroy(e);
     for (auto e : ev_free) cudaEventDestroy(e);
   }
-  int64_t factor_bytes = 0;
-
   template <class T>
   const T* upload(const std::vector<T>& v) {
     auto b = std::make_unique<DevBuf>();
@@ -374,6 +380,7 @@ void launch_chain_t(const ChainArgs& a, bool fwd, cudaStream_t st) {
 }
 
 void launch_chain(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
+  if (a.nr <= 0) return;
   switch (mp) {
     case 8: launch_chain_t<8, 32, 1, 4>(a, fwd, st); break;
     case 16: launch_chain_t<16, 16, 1, 1>(a, fwd, st); break;
@@ -392,9 +399,24 @@ int64_t pad_order(int64_t m, int mode) {
   return (m + 7) / 8 * 8;
 }
 
-// ---------------------------------------------------------------- plan build
-void build_plan(btd_plan& pl, const double* diag, const double* lower, const double* upper, int flags,
-                cudaStream_t st, int64_t* err_row) {
+// f~_q = base_q + carry_{q-1}  from the all-gathered (base, carry) pairs
+__global__ void assemble_ft_kernel(const double* exch, double* ft, int64_t nr, int64_t mpK) {
+  const int64_t total = nr * mpK;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / mpK, r = e % mpK;
+    double v = exch[(2 * q) * mpK + r];
+    if (q >= 1) v += exch[(2 * (q - 1) + 1) * mpK + r];
+    ft[e] = v;
+  }
+}
+
+// ---------------------------------------------------------------- plan build, local part
+// Ranges owned by this rank: [q0, q1).  The rank reads only its rows of the
+// matrix and produces its factors plus the four reduced-system contributions
+// per range; the tree part (build_finish) needs everyone's contributions.
+void build_local(btd_plan& pl, const double* diag, const double* lower, const double* upper, int flags,
+                 cudaStream_t st, int64_t* err_row, int64_t* err_range) {
   const int64_t n = pl.n, m = pl.m;
   int forced = -1;
   if (const char* e = getenv("BTD_FORCE_MODE")) forced = atoi(e);
@@ -403,55 +425,62 @@ void build_plan(btd_plan& pl, const double* diag, const double* lower, const dou
   const int64_t mp = pl.mp, blk = mp * mp;
   pl.blk = blk;
   pl.nr = std::min<int64_t>(n, pl.ranks * std::max<int64_t>(1, pl.split));
+  if (pl.world > 1 && pl.nr % pl.world != 0)
+    fail(BTD_ERR_INVALID_ARG, "device ranges (ranks*split) must be a multiple of the world size");
   pl.L = (n + pl.nr - 1) / pl.nr;
   pl.npad = pl.L * pl.nr;
   pl.cap = pl.L - 1;
-  const int64_t nr = pl.nr, L = pl.L, npad = pl.npad, cap = pl.cap;
-  pl.lo.resize(nr);
-  pl.slot0.resize(nr);
-  pl.nint.resize(nr);
+  pl.nrl = pl.nr / pl.world;
+  pl.q0 = pl.rank * pl.nrl;
+  pl.q1 = pl.q0 + pl.nrl;
+  pl.R0 = pl.q0 * pl.L;
+  pl.nl = pl.nrl * pl.L;
+  pl.nloc = std::max<int64_t>(0, std::min<int64_t>(pl.nl, n - pl.R0));
+  const int64_t nrl = pl.nrl, L = pl.L, cap = pl.cap, nl = pl.nl, R0 = pl.R0, nr = pl.nr;
+  pl.lo.resize(nrl);
+  pl.slot0.resize(nrl);
+  pl.nint.resize(nrl);
   pl.nlive = 0;
-  for (int64_t q = 0; q < nr; ++q) {
-    pl.lo[q] = q * L;
-    pl.slot0[q] = q * cap;
-    pl.nint[q] = (int32_t)std::max<int64_t>(0, std::min<int64_t>(L - 1, n - q * L - 1));
-    if (q * L < n) pl.nlive++;
+  for (int64_t ql = 0; ql < nrl; ++ql) {
+    const int64_t glo = (pl.q0 + ql) * L;
+    pl.lo[ql] = ql * L;
+    pl.slot0[ql] = ql * cap;
+    pl.nint[ql] = (int32_t)std::max<int64_t>(0, std::min<int64_t>(L - 1, n - glo - 1));
+    if (glo < n) pl.nlive++;
   }
   pl.d_lo = pl.upload(pl.lo);
   pl.d_slot0 = pl.upload(pl.slot0);
   pl.d_nint = pl.upload(pl.nint);
-  std::vector<int64_t> iota(nr + 1);
-  for (int64_t i = 0; i <= nr; ++i) iota[i] = i;
-  pl.d_qiota = pl.upload(iota);
 
-  // ---- padded matrix: [C (npad) | Lw (npad) | Uw (npad)] blocks
+  // ---- local padded matrix rows [R0, R0+nl): [C | Lw | Uw], nl blocks each
+  //      Lw[i] = lower[R0+i] (couples row R0+i+1 to R0+i), Uw[i] = upper[R0+i]; zero / identity past n
   DevBuf mat, tmp;
-  mat.alloc((size_t)3 * npad * blk * sizeof(double));
+  mat.alloc((size_t)3 * nl * blk * sizeof(double));
   {
     const double* srcs[3] = {diag, lower, upper};
-    const int64_t counts[3] = {n, n - 1, n - 1};
+    const int64_t counts[3] = {std::max<int64_t>(0, std::min(nl, n - R0)), std::max<int64_t>(0, std::min(nl, n - 1 - R0)),
+                               std::max<int64_t>(0, std::min(nl, n - 1 - R0))};
     const bool on_dev = flags & BTD_MATRIX_ON_DEVICE;
-    size_t maxb = (size_t)n * m * m * sizeof(double);
-    if (!on_dev) tmp.alloc(maxb);
+    if (!on_dev) tmp.alloc((size_t)nl * m * m * sizeof(double));
     for (int s = 0; s < 3; ++s) {
-      const double* src = srcs[s];
+      const double* src = srcs[s] ? srcs[s] + (size_t)R0 * m * m : nullptr;
       const size_t bytes = (size_t)counts[s] * m * m * sizeof(double);
       if (!on_dev && bytes) {
         CK(cudaMemcpyAsync(tmp.p, src, bytes, cudaMemcpyHostToDevice, st));
         src = tmp.d();
       }
-      pad_blocks_kernel<<<1184, 256, 0, st>>>(src, counts[s], (int)m, mat.d() + (size_t)s * npad * blk, npad,
-                                             (int)mp, s == 0);
+      pad_blocks_kernel<<<1184, 256, 0, st>>>(src, counts[s], (int)m, mat.d() + (size_t)s * nl * blk, nl, (int)mp,
+                                             s == 0);
       CK_LAUNCH();
       if (!on_dev) CK(cudaStreamSynchronize(st));  // tmp reused
     }
   }
   tmp.release();
   const double* Cm = mat.d();
-  const int64_t offL = npad, offU = 2 * npad;
+  const int64_t offL = nl, offU = 2 * nl;
 
-  // ---- pool layout
-  const int64_t nslot = nr * cap;
+  // ---- pool layout: local factors, global reduced system, constants
+  const int64_t nslot = nrl * cap;
   int64_t o = 0;
   auto take = [&](int64_t cnt) { int64_t r = o; o += cnt; return r; };
   pl.off_AD = take(nslot);
@@ -459,11 +488,11 @@ void build_plan(btd_plan& pl, const double* diag, const double* lower, const dou
   pl.off_S = take(nslot);
   pl.off_G = take(nslot);
   pl.off_Tb = take(nslot);
-  pl.off_Fc = take(nr);
-  pl.off_Bif = take(nr);
-  pl.off_BU = take(nr);
-  pl.off_BV = take(nr);
-  pl.off_Dt = take(nr);
+  pl.off_Fc = take(nrl);
+  pl.off_Bif = take(nrl);
+  pl.off_BU = take(nrl);
+  pl.off_BV = take(nrl);
+  pl.off_Dt = take(nrl);
   pl.off_Rd = take(nr);
   pl.off_Rl = take(nr);
   pl.off_Ru = take(nr);
@@ -482,47 +511,46 @@ void build_plan(btd_plan& pl, const double* diag, const double* lower, const dou
   const int64_t* lo_arr = pl.d_lo;
   const int64_t* slot_arr = pl.d_slot0;
   DevBuf ws, fail_step, fail_col;
-  fail_step.alloc(sizeof(int32_t) * std::max<int64_t>(nr, 1));
-  fail_col.alloc(sizeof(int32_t) * std::max<int64_t>(nr, 1));
-  CK(cudaMemsetAsync(fail_step.p, 0xff, sizeof(int32_t) * nr, st));
+  fail_step.alloc(sizeof(int32_t) * std::max<int64_t>(nrl, 1));
+  fail_col.alloc(sizeof(int32_t) * std::max<int64_t>(nrl, 1));
+  CK(cudaMemsetAsync(fail_step.p, 0xff, sizeof(int32_t) * std::max<int64_t>(nrl, 1), st));
 
-  // Bif_q = upper[lo_q], Fc_q = lower[hi_q - 1]  (padded arrays; zero past n)
+  // Bif_q = upper[lo_q], Fc_q = lower[hi_q - 1]
   {
-    std::vector<int64_t> src(2 * nr), dst(2 * nr);
-    for (int64_t q = 0; q < nr; ++q) {
+    std::vector<int64_t> src(2 * nrl), dst(2 * nrl);
+    for (int64_t q = 0; q < nrl; ++q) {
       src[q] = offU + pl.lo[q];
       dst[q] = pl.off_Bif + q;
-      src[nr + q] = offL + (q + 1) * L - 1;
-      dst[nr + q] = pl.off_Fc + q;
+      src[nrl + q] = offL + (q + 1) * L - 1;
+      dst[nrl + q] = pl.off_Fc + q;
     }
-    const int64_t* s_ = pl.upload(src);
-    const int64_t* d_ = pl.upload(dst);
-    launch_gemm(mp, mp, (int)(2 * nr), mk(pool, d_, 0, blk, mp), mk(Cm, s_, 0, blk, mp), 1.0, {}, st);
+    launch_gemm(mp, mp, (int)(2 * nrl), mk(pool, pl.upload(dst), 0, blk, mp), mk(Cm, pl.upload(src), 0, blk, mp), 1.0,
+                {}, st);
   }
 
-  if (cap > 0) {
-    std::vector<int64_t> sa_c(2 * nr), sa_a(2 * nr), sa_b(2 * nr), gt_c(2 * nr), gt_a0(2 * nr),
-        gt_a(2 * nr), gt_b(2 * nr);
-    for (int64_t q = 0; q < nr; ++q) {
+  const int nb = (int)nrl;
+  if (cap > 0 && nb > 0) {
+    std::vector<int64_t> sa_c(2 * nrl), sa_a(2 * nrl), sa_b(2 * nrl), gt_c(2 * nrl), gt_a0(2 * nrl),
+        gt_a(2 * nrl), gt_b(2 * nrl);
+    for (int64_t q = 0; q < nrl; ++q) {
       const int64_t s0 = pl.slot0[q];
       sa_c[q] = pl.off_S + s0;
-      sa_c[nr + q] = pl.off_AD + s0;
-      sa_a[q] = sa_a[nr + q] = pl.off_Dinv + s0;
+      sa_c[nrl + q] = pl.off_AD + s0;
+      sa_a[q] = sa_a[nrl + q] = pl.off_Dinv + s0;
       sa_b[q] = offU + pl.lo[q] + 1;   // B_g = upper[g], g = lo+1+j
-      sa_b[nr + q] = offL + pl.lo[q];  // A_g = lower[g-1]
+      sa_b[nrl + q] = offL + pl.lo[q];  // A_g = lower[g-1]
       gt_c[q] = pl.off_G + s0;
-      gt_c[nr + q] = pl.off_Tb + s0;
-      gt_a0[q] = pl.off_AD + s0;       // G_0 = AD_0
-      gt_a0[nr + q] = pl.off_Bif + q;  // Tb_0 = B_lo
-      gt_a[q] = pl.off_AD + s0;        // G_j = AD_j G_{j-1}
-      gt_a[nr + q] = pl.off_Tb + s0 - 1;  // Tb_j = Tb_{j-1} S_{j-1}
+      gt_c[nrl + q] = pl.off_Tb + s0;
+      gt_a0[q] = pl.off_AD + s0;          // G_0 = AD_0
+      gt_a0[nrl + q] = pl.off_Bif + q;    // Tb_0 = B_lo
+      gt_a[q] = pl.off_AD + s0;           // G_j = AD_j G_{j-1}
+      gt_a[nrl + q] = pl.off_Tb + s0 - 1;  // Tb_j = Tb_{j-1} S_{j-1}
       gt_b[q] = pl.off_G + s0 - 1;
-      gt_b[nr + q] = pl.off_S + s0 - 1;
+      gt_b[nrl + q] = pl.off_S + s0 - 1;
     }
     const int64_t *d_sa_c = pl.upload(sa_c), *d_sa_a = pl.upload(sa_a), *d_sa_b = pl.upload(sa_b),
                   *d_gt_c = pl.upload(gt_c), *d_gt_a0 = pl.upload(gt_a0), *d_gt_a = pl.upload(gt_a),
                   *d_gt_b = pl.upload(gt_b);
-    const int nb = (int)nr;
     for (int64_t j = 0; j < cap; ++j) {
       // D_j = C_g - A_g S_{j-1}     (ref _kernels.pyx:168)
       if (j == 0)
@@ -558,46 +586,102 @@ void build_plan(btd_plan& pl, const double* diag, const double* lower, const dou
 
   // ---- range failures: first range (in order) wins, row local to its interior
   {
-    std::vector<int32_t> fs(nr);
-    CK(cudaMemcpyAsync(fs.data(), fail_step.p, sizeof(int32_t) * nr, cudaMemcpyDeviceToHost, st));
+    std::vector<int32_t> fs(std::max<int64_t>(nrl, 1), -1);
+    if (nrl) CK(cudaMemcpyAsync(fs.data(), fail_step.p, sizeof(int32_t) * nrl, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    for (int64_t q = 0; q < nr; ++q)
+    for (int64_t q = 0; q < nrl; ++q)
       if (fs[q] >= 0) {
         *err_row = fs[q];
+        *err_range = pl.q0 + q;
         char buf[160];
-        snprintf(buf, sizeof buf, "block row %d: singular pivot (range %lld)", fs[q], (long long)q);
+        snprintf(buf, sizeof buf, "block row %d: singular pivot (range %lld)", fs[q], (long long)(pl.q0 + q));
         fail(BTD_ERR_SINGULAR_PIVOT, buf);
       }
   }
 
-  // ---- reduced system (ref dichotomy.py:212-236)
+  // ---- per-range contributions to the reduced system (ref dichotomy.py:212-236)
+  //   c0 = C_lo - B_lo U[1]     (own diagonal)
+  //   c1 = A_{hi} V[L-1]        (subtracted from the NEXT range's diagonal)
+  //   c2 = A_{hi} U[L-1]        (the next range's lower coupling)
+  //   c3 = B_lo V[1]            (own upper coupling)
+  pl.contrib.alloc((size_t)std::max<int64_t>(nrl, 1) * 4 * blk * sizeof(double));
+  if (nrl) {
+    double* cb = pl.contrib.d();
+    std::vector<int64_t> c0c(nrl), c0in(nrl), c0a(nrl), c1c(nrl), c1a(nrl), c1b(nrl), c2c(nrl), c2b(nrl),
+        c3c(nrl), c3in(nrl);
+    for (int64_t q = 0; q < nrl; ++q) {
+      c0c[q] = 4 * q; c0in[q] = pl.lo[q]; c0a[q] = pl.off_BU + q;
+      c1c[q] = 4 * q + 1; c1a[q] = pl.off_Fc + q;
+      c1b[q] = cap > 0 ? pl.off_S + pl.slot0[q] + cap - 1 : pl.off_Z;
+      c2c[q] = 4 * q + 2; c2b[q] = cap > 0 ? pl.off_G + pl.slot0[q] + cap - 1 : pl.off_I;
+      c3c[q] = 4 * q + 3; c3in[q] = cap > 0 ? pl.off_BV + q : pl.off_Bif + q;
+    }
+    const int64_t* dI = nullptr;
+    (void)dI;
+    launch_gemm(mp, mp, nb, mk(cb, pl.upload(c0c), 0, blk, mp), mk(Cm, pl.upload(c0in), 0, blk, mp), 1.0,
+                {term(mk(pool, pl.upload(c0a), 0, blk, mp), mk(pool + pl.off_I * blk, nullptr, 0, 0, mp), mp, -1.0)},
+                st);
+    const int64_t* d_c1a = pl.upload(c1a);
+    launch_gemm(mp, mp, nb, mk(cb, pl.upload(c1c), 0, blk, mp), none(), 0.0,
+                {term(mk(pool, d_c1a, 0, blk, mp), mk(pool, pl.upload(c1b), 0, blk, mp), mp)}, st);
+    launch_gemm(mp, mp, nb, mk(cb, pl.upload(c2c), 0, blk, mp), none(), 0.0,
+                {term(mk(pool, d_c1a, 0, blk, mp), mk(pool, pl.upload(c2b), 0, blk, mp), mp)}, st);
+    launch_gemm(mp, mp, nb, mk(cb, pl.upload(c3c), 0, blk, mp), mk(pool, pl.upload(c3in), 0, blk, mp), 1.0, {}, st);
+  }
+  mat.release();
+
+  // ---- solve-time local batches
   {
-    std::vector<int64_t> rd_c(nr), rd_in(nr), t1a(nr), t1b(nr), t2a(nr), rl_c, rl_a, rl_b, ru_c, ru_a;
-    for (int64_t q = 0; q < nr; ++q) {
-      rd_c[q] = pl.off_Rd + q;
-      rd_in[q] = pl.lo[q];
-      t1a[q] = q >= 1 ? pl.off_Fc + q - 1 : pl.off_Z;
-      t1b[q] = (q >= 1 && cap > 0) ? pl.off_S + pl.slot0[q - 1] + cap - 1 : pl.off_Z;
-      t2a[q] = pl.off_BU + q;
-      if (q >= 1) {
-        rl_c.push_back(pl.off_Rl + q - 1);
-        rl_a.push_back(pl.off_Fc + q - 1);
-        rl_b.push_back(cap > 0 ? pl.off_G + pl.slot0[q - 1] + cap - 1 : pl.off_I);
+    // carry_q = Fc_q y_{q,last}: ranges whose last interior row lies inside [0, n)
+    std::vector<int64_t> cs, cf, cr;
+    for (int64_t q = 0; q < nrl; ++q)
+      if (cap > 0 && pl.nint[q] == cap && (pl.q0 + q + 1) * L <= n && pl.q0 + q + 1 < nr) {
+        cs.push_back(q); cf.push_back(pl.off_Fc + q); cr.push_back(pl.lo[q] + L - 1);
       }
-      if (q <= nr - 2) {
-        ru_c.push_back(pl.off_Ru + q);
-        ru_a.push_back(cap > 0 ? pl.off_BV + q : pl.off_Bif + q);
+    pl.ncarry = (int)cs.size();
+    pl.carry_src = pl.upload(cs); pl.carry_fc = pl.upload(cf); pl.carry_row = pl.upload(cr);
+    if (pl.mode == 1) {
+      pl.steps1.resize(cap);
+      for (int64_t j = 0; j < cap; ++j) {
+        std::vector<int64_t> xr, xs, xq, tr, ts, tq;
+        int cnt = 0;
+        for (int64_t q = 0; q < nrl; ++q) {
+          if (pl.nint[q] > j) ++cnt;
+          if (j < pl.nint[q] - 1) { xr.push_back(pl.lo[q] + 1 + j); xs.push_back(pl.slot0[q] + j); xq.push_back(q); }
+          else if (j == pl.nint[q] - 1) { tr.push_back(pl.lo[q] + 1 + j); ts.push_back(pl.slot0[q] + j); tq.push_back(q); }
+        }
+        auto& s = pl.steps1[j];
+        s.cnt = cnt; s.nx = (int)xq.size(); s.nt = (int)tq.size();
+        s.x_row = pl.upload(xr); s.x_slot = pl.upload(xs); s.x_q = pl.upload(xq);
+        s.t_row = pl.upload(tr); s.t_slot = pl.upload(ts); s.t_q = pl.upload(tq);
       }
     }
-    launch_gemm(mp, mp, (int)nr, mk(pool, pl.upload(rd_c), 0, blk, mp), mk(Cm, pl.upload(rd_in), 0, blk, mp), 1.0,
-                {term(mk(pool, pl.upload(t1a), 0, blk, mp), mk(pool, pl.upload(t1b), 0, blk, mp), mp, -1.0),
-                 term(mk(pool, pl.upload(t2a), 0, blk, mp), mk(pool + pl.off_I * blk, nullptr, 0, 0, mp), mp, -1.0)},
-                st);
-    if (!rl_c.empty()) {
-      launch_gemm(mp, mp, (int)rl_c.size(), mk(pool, pl.upload(rl_c), 0, blk, mp), none(), 0.0,
-                  {term(mk(pool, pl.upload(rl_a), 0, blk, mp), mk(pool, pl.upload(rl_b), 0, blk, mp), mp)}, st);
-      launch_gemm(mp, mp, (int)ru_c.size(), mk(pool, pl.upload(ru_c), 0, blk, mp),
-                  mk(pool, pl.upload(ru_a), 0, blk, mp), 1.0, {}, st);
+  }
+  CK(cudaStreamSynchronize(st));
+}
+
+// ---------------------------------------------------------------- plan build, global part
+// contrib_all: [nr][4][mp][mp] device, identical on every rank.
+void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int64_t* err_row) {
+  const int64_t mp = pl.mp, blk = pl.blk, nr = pl.nr;
+  double* pool = pl.pool.d();
+  const double* I = pool + pl.off_I * blk;
+  // reduced system: Rd_q = c0_q - c1_{q-1}, Rl_{q-1} = c2_{q-1}, Ru_q = c3_q
+  {
+    std::vector<int64_t> d_c, d_in, d_a, l_c, l_in, u_c, u_in;
+    for (int64_t q = 0; q < nr; ++q) {
+      if (q >= 1) { d_c.push_back(pl.off_Rd + q); d_in.push_back(4 * q); d_a.push_back(4 * (q - 1) + 1); }
+      if (q >= 1) { l_c.push_back(pl.off_Rl + q - 1); l_in.push_back(4 * (q - 1) + 2); }
+      if (q + 1 < nr) { u_c.push_back(pl.off_Ru + q); u_in.push_back(4 * q + 3); }
+    }
+    launch_gemm(mp, mp, 1, mk(pool, nullptr, pl.off_Rd, blk, mp), mk(contrib_all, nullptr, 0, blk, mp), 1.0, {}, st);
+    if (!d_c.empty()) {
+      launch_gemm(mp, mp, (int)d_c.size(), mk(pool, pl.upload(d_c), 0, blk, mp), mk(contrib_all, pl.upload(d_in), 0, blk, mp),
+                  1.0, {term(mk(contrib_all, pl.upload(d_a), 0, blk, mp), mk(I, nullptr, 0, 0, mp), mp, -1.0)}, st);
+      launch_gemm(mp, mp, (int)l_c.size(), mk(pool, pl.upload(l_c), 0, blk, mp), mk(contrib_all, pl.upload(l_in), 0, blk, mp),
+                  1.0, {}, st);
+      launch_gemm(mp, mp, (int)u_c.size(), mk(pool, pl.upload(u_c), 0, blk, mp), mk(contrib_all, pl.upload(u_in), 0, blk, mp),
+                  1.0, {}, st);
     }
     // transposed system T = R^T: diag Rd^T, lower Ru^T, upper Rl^T (ref core.py:137-143)
     std::vector<int64_t> ti, to;
@@ -613,7 +697,6 @@ void build_plan(btd_plan& pl, const double* diag, const double* lower, const dou
     transpose_blocks_kernel<<<grid, dim3(32, 8), 0, st>>>(pool, pl.upload(ti), pool, pl.upload(to), nb, (int)mp);
     CK_LAUNCH();
   }
-  mat.release();
 
   // ---- partition tree inverse rows (ref dichotomy.py:134-146, 298-304)
   pl.nodes = partition_tree(nr, &pl.depth);
@@ -632,8 +715,7 @@ void build_plan(btd_plan& pl, const double* diag, const double* lower, const dou
     maxlevel = std::max(maxlevel, pl.nodes[b].level);
   }
   eoff[nn] = rtot;
-  // tree pool: Dp, Sp, ADp, Y (tot each) + Dt scratch (nn)
-  DevBuf tp, tfs, tfc;
+  DevBuf tp, tfs, tfc, ws;
   const int64_t tpD = 0, tpS = tot, tpAD = 2 * tot, tpY = 3 * tot, tpDt = 4 * tot;
   tp.alloc((size_t)(4 * tot + nn) * blk * sizeof(double));
   CK(cudaMemsetAsync(tp.p, 0, (size_t)(4 * tot + nn) * blk * sizeof(double), st));
@@ -646,17 +728,15 @@ void build_plan(btd_plan& pl, const double* diag, const double* lower, const dou
     int64_t smax = 0;
     for (int b = 0; b < nn; ++b)
       if (pl.nodes[b].level == lev) { ids.push_back(b); smax = std::max(smax, sz[b]); }
-    // factor D'_i, S'_i, AD'_i for i = 0..smax-1 (transposed system, batched over nodes)
     for (int64_t i = 0; i < smax; ++i) {
-      std::vector<int64_t> dt_c, dt_in, dt_a, dt_b, inv_in, inv_out, sc, sa, sb, ac, aa, ab;
-      std::vector<int64_t> failidx;
+      std::vector<int64_t> dt_c, dt_in, dt_a, dt_b, inv_in, inv_out, sc, sa, sb, ac, aa, ab, failidx;
       for (int b : ids) {
         if (sz[b] <= i) continue;
         const int64_t lo = pl.nodes[b].lo;
         dt_c.push_back(tpDt + b);
         dt_in.push_back(pl.off_RdT + lo + i);
         dt_a.push_back(i >= 1 ? pl.off_RuT + lo + i - 1 : pl.off_Z);
-        dt_b.push_back(i >= 1 ? tpS + nb0[b] + i - 1 : -1);
+        dt_b.push_back(i >= 1 ? tpS + nb0[b] + i - 1 : 0);
         inv_in.push_back(tpDt + b);
         inv_out.push_back(tpD + nb0[b] + i);
         failidx.push_back(b);
@@ -668,14 +748,11 @@ void build_plan(btd_plan& pl, const double* diag, const double* lower, const dou
         }
       }
       const int cnt = (int)dt_c.size();
-      // D'_i into tree-pool scratch; operands from two pools -> stage via pool copy when i >= 1
-      if (i == 0) {
-        launch_gemm(mp, mp, cnt, mk(T, pl.upload(dt_c), 0, blk, mp), mk(pool, pl.upload(dt_in), 0, blk, mp), 1.0, {},
-                    st);
-      } else {
+      if (i == 0)
+        launch_gemm(mp, mp, cnt, mk(T, pl.upload(dt_c), 0, blk, mp), mk(pool, pl.upload(dt_in), 0, blk, mp), 1.0, {}, st);
+      else
         launch_gemm(mp, mp, cnt, mk(T, pl.upload(dt_c), 0, blk, mp), mk(pool, pl.upload(dt_in), 0, blk, mp), 1.0,
                     {term(mk(pool, pl.upload(dt_a), 0, blk, mp), mk(T, pl.upload(dt_b), 0, blk, mp), mp, -1.0)}, st);
-      }
       launch_inv(pl, cnt, T, pl.upload(inv_in), 0, T, pl.upload(inv_out), 0, (int)i, tfs.i32(), tfc.i32(), ws, st,
                  pl.upload(failidx));
       if (!sc.empty())
@@ -695,8 +772,7 @@ void build_plan(btd_plan& pl, const double* diag, const double* lower, const dou
         else if (i > kk) { gc.push_back(tpY + nb0[b] + i); ga.push_back(tpAD + nb0[b] + i); gb.push_back(tpY + nb0[b] + i - 1); }
       }
       if (!cc.empty())
-        launch_gemm(mp, mp, (int)cc.size(), mk(T, pl.upload(cc), 0, blk, mp), mk(T, pl.upload(ci), 0, blk, mp), 1.0, {},
-                    st);
+        launch_gemm(mp, mp, (int)cc.size(), mk(T, pl.upload(cc), 0, blk, mp), mk(T, pl.upload(ci), 0, blk, mp), 1.0, {}, st);
       if (!gc.empty())
         launch_gemm(mp, mp, (int)gc.size(), mk(T, pl.upload(gc), 0, blk, mp), none(), 0.0,
                     {term(mk(T, pl.upload(ga), 0, blk, mp), mk(T, pl.upload(gb), 0, blk, mp), mp)}, st);
@@ -715,8 +791,7 @@ void build_plan(btd_plan& pl, const double* diag, const double* lower, const dou
       }
     }
   }
-  // tree failures: first node in BFS order
-  {
+  {  // tree failures: first node in BFS order (ref dichotomy.py:298-304 loop order)
     std::vector<int32_t> fs(nn);
     CK(cudaMemcpyAsync(fs.data(), tfs.p, sizeof(int32_t) * nn, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -760,17 +835,35 @@ void build_plan(btd_plan& pl, const double* diag, const double* lower, const dou
                   {term(mk(pl.Rrows.d(), pl.upload(ha), 0, 1, 0, pl.upload(hld)), mk(pool, pl.upload(hb), 0, blk, mp), mp)},
                   st);
   }
-  // solve-time level batches
-  {
+  {  // solve-time batches over the nodes this rank needs
+    // x~ needed for own interfaces q0..q1-1 and the right neighbour q1; node k needs x~_{lo-1}, x~_{hi+1}
+    std::vector<char> need_k(nr + 1, 0);
+    for (int64_t q = pl.q0; q <= std::min(pl.q1, nr - 1); ++q) need_k[q] = 1;
+    std::vector<int> node_of_k(nr, -1);
+    for (int b = 0; b < nn; ++b) node_of_k[pl.nodes[b].k] = b;
+    for (bool changed = true; changed;) {
+      changed = false;
+      for (int b = nn - 1; b >= 0; --b) {
+        const Node& nd = pl.nodes[b];
+        if (!need_k[nd.k]) continue;
+        if (nd.lo >= 1 && !need_k[nd.lo - 1]) { need_k[nd.lo - 1] = 1; changed = true; }
+        if (nd.hi + 1 <= nr - 1 && !need_k[nd.hi + 1]) { need_k[nd.hi + 1] = 1; changed = true; }
+      }
+    }
+    std::vector<int64_t> zid, zro, zrl, znl;
+    for (int b = 0; b < nn; ++b)
+      if (need_k[pl.nodes[b].k]) { zid.push_back(b); zro.push_back(roff[b]); zrl.push_back(rld[b]); znl.push_back(pl.nodes[b].lo); }
+    pl.nz = (int)zid.size();
+    pl.z_id = pl.upload(zid); pl.z_roff = pl.upload(zro); pl.z_rld = pl.upload(zrl); pl.z_nlo = pl.upload(znl);
     std::vector<int64_t> nlo(nn);
     for (int b = 0; b < nn; ++b) nlo[b] = pl.nodes[b].lo;
     pl.d_nlo = pl.upload(nlo);
-    pl.levels.resize(maxlevel + 1);
+    pl.levels.assign(maxlevel + 1, btd_plan::Level());
     for (int64_t lev = 0; lev <= maxlevel; ++lev) {
       std::vector<int64_t> c, z, e, xl, h, xh;
       for (int b = 0; b < nn; ++b) {
         const Node& nd = pl.nodes[b];
-        if (nd.level != lev) continue;
+        if (nd.level != lev || !need_k[nd.k]) continue;
         c.push_back(nd.k); z.push_back(b); e.push_back(2 * b); h.push_back(2 * b + 1);
         xl.push_back(nd.lo >= 1 ? nd.lo - 1 : nr);
         xh.push_back(nd.hi + 1 <= nr - 1 ? nd.hi + 1 : nr);
@@ -780,127 +873,196 @@ void build_plan(btd_plan& pl, const double* diag, const double* lower, const dou
       L_.c_idx = pl.upload(c); L_.z_idx = pl.upload(z); L_.e_idx = pl.upload(e);
       L_.xl_idx = pl.upload(xl); L_.h_idx = pl.upload(h); L_.xh_idx = pl.upload(xh);
     }
-    // interface RHS carry: f~_q += Fc_{q-1} y_{q-1,last} for ranges q-1 entirely inside [0,n)
-    std::vector<int64_t> cq, cf, cr;
-    for (int64_t q = 1; q < nr; ++q)
-      if (cap > 0 && pl.lo[q] <= n && pl.nint[q - 1] == cap) {
-        cq.push_back(q); cf.push_back(pl.off_Fc + q - 1); cr.push_back(pl.lo[q] - 1);
-      }
-    pl.ncarry = (int)cq.size();
-    pl.carry_q = pl.upload(cq); pl.carry_fc = pl.upload(cf); pl.carry_row = pl.upload(cr);
-    // mode-1 step batches
-    if (pl.mode == 1) {
-      pl.steps1.resize(cap);
-      for (int64_t j = 0; j < cap; ++j) {
-        std::vector<int64_t> xr, xs, xq, tr, ts, tq;
-        int cnt = 0;
-        for (int64_t q = 0; q < nr; ++q) {
-          if (pl.nint[q] > j) ++cnt;
-          if (j < pl.nint[q] - 1) { xr.push_back(pl.lo[q] + 1 + j); xs.push_back(pl.slot0[q] + j); xq.push_back(q); }
-          else if (j == pl.nint[q] - 1) { tr.push_back(pl.lo[q] + 1 + j); ts.push_back(pl.slot0[q] + j); tq.push_back(q); }
-        }
-        auto& s = pl.steps1[j];
-        s.cnt = cnt; s.nx = (int)xq.size(); s.nt = (int)tq.size();
-        s.x_row = pl.upload(xr); s.x_slot = pl.upload(xs); s.x_q = pl.upload(xq);
-        s.t_row = pl.upload(tr); s.t_slot = pl.upload(ts); s.t_q = pl.upload(tq);
-      }
-    }
   }
   CK(cudaStreamSynchronize(st));
   pl.factor_bytes += (int64_t)(rtot + 2 * nn * blk) * sizeof(double);
+  pl.finished = true;
 }
 
 // ---------------------------------------------------------------- solve
 void ensure_scratch(btd_plan& pl, int64_t K) {
   if (pl.scratch_k == K) return;
   const int64_t mpK = pl.mp * K;
-  pl.base.alloc((size_t)pl.nr * mpK * sizeof(double));
+  pl.ft.alloc((size_t)pl.nr * mpK * sizeof(double));
   pl.zbuf.alloc((size_t)pl.nodes.size() * mpK * sizeof(double));
   pl.xt.alloc((size_t)(pl.nr + 1) * mpK * sizeof(double));
   CK(cudaMemset(pl.xt.p, 0, (size_t)(pl.nr + 1) * mpK * sizeof(double)));
-  CK(cudaMemset(pl.base.p, 0, (size_t)pl.nr * mpK * sizeof(double)));
+  CK(cudaMemset(pl.ft.p, 0, (size_t)pl.nr * mpK * sizeof(double)));
   pl.scratch_k = K;
 }
 
-void solve_device(btd_plan& pl, const double* F, double* X, int64_t K, cudaStream_t st) {
-  const int64_t mp = pl.mp, m = pl.m, blk = pl.blk, nr = pl.nr;
-  const int64_t mpK = mp * K, mK = m * K;
+ChainArgs chain_args(btd_plan& pl, const double* F, double* X, int64_t K, double* base, int64_t base_stride) {
+  const int64_t blk = pl.blk;
   double* pool = pl.pool.d();
-  double* base = pl.base.d();
+  ChainArgs a;
+  a.lo = pl.d_lo; a.nint = pl.d_nint; a.slot0 = pl.d_slot0; a.nr = (int)pl.nrl;
+  a.m = (int)pl.m; a.n = pl.nloc; a.K = K; a.F = F; a.X = X;
+  a.AD = pool + pl.off_AD * blk; a.Dinv = pool + pl.off_Dinv * blk; a.Tb = pool + pl.off_Tb * blk;
+  a.S = pool + pl.off_S * blk; a.G = pool + pl.off_G * blk;
+  a.base = base; a.base_stride = base_stride;
+  a.xt = pl.xt.d() + pl.q0 * pl.mp * K;
+  return a;
+}
+
+// Forward sweeps of the owned ranges: y rows into X, base_q into base (+ q*base_stride)
+void solve_forward(btd_plan& pl, const double* F, double* X, int64_t K, double* base, int64_t base_stride,
+                   cudaStream_t st) {
+  const int64_t mp = pl.mp, m = pl.m, blk = pl.blk;
+  const int64_t mK = m * K;
+  double* pool = pl.pool.d();
+  if (pl.mode == 0) {
+    launch_chain(mp, chain_args(pl, F, X, K, base, base_stride), true, st);
+    return;
+  }
+  // mode 1: base_q = F[lo_q] (rows < m; pad rows stay 0), then one GEMM launch per row step
+  launch_gemm(m, K, pl.nlive, mk(base, nullptr, 0, base_stride, K), mk(F, pl.d_lo, 0, mK, K), 1.0, {}, st);
+  for (int64_t j = 0; j < pl.cap; ++j) {
+    const auto& s = pl.steps1[j];
+    if (s.cnt == 0) break;
+    if (j == 0)
+      launch_gemm(m, K, s.cnt, mk(X, pl.d_lo, 1, mK, K), none(), 0.0,
+                  {term(mk(pool, pl.d_slot0, pl.off_Dinv, blk, mp), mk(F, pl.d_lo, 1, mK, K), m)}, st);
+    else
+      launch_gemm(m, K, s.cnt, mk(X, pl.d_lo, 1 + j, mK, K), none(), 0.0,
+                  {term(mk(pool, pl.d_slot0, pl.off_Dinv + j, blk, mp), mk(F, pl.d_lo, 1 + j, mK, K), m),
+                   term(mk(pool, pl.d_slot0, pl.off_AD + j, blk, mp), mk(X, pl.d_lo, j, mK, K), m)},
+                  st);
+    launch_gemm(mp, K, s.cnt, mk(base, nullptr, 0, base_stride, K), mk(base, nullptr, 0, base_stride, K), 1.0,
+                {term(mk(pool, pl.d_slot0, pl.off_Tb + j, blk, mp), mk(X, pl.d_lo, 1 + j, mK, K), m)}, st);
+  }
+}
+
+// Algorithm 1 on the interface system: z = R f~ (all nodes), then the levels.
+void solve_tree(btd_plan& pl, int64_t K, cudaStream_t st) {
+  const int64_t mp = pl.mp, blk = pl.blk, mpK = mp * K;
+  double* ft = pl.ft.d();
   double* xt = pl.xt.d();
   double* z = pl.zbuf.d();
-  pl.ev_mark(0, st);
-  if (pl.mode == 0) {
-    ChainArgs a;
-    a.lo = pl.d_lo; a.nint = pl.d_nint; a.slot0 = pl.d_slot0; a.nr = (int)nr;
-    a.m = (int)m; a.n = pl.n; a.K = K; a.F = F; a.X = X;
-    a.AD = pool + pl.off_AD * blk; a.Dinv = pool + pl.off_Dinv * blk; a.Tb = pool + pl.off_Tb * blk;
-    a.S = pool + pl.off_S * blk; a.G = pool + pl.off_G * blk;
-    a.base = base; a.xt = xt;
-    launch_chain(mp, a, true, st);
-  } else {
-    // mode 1: base_q = F[lo_q] (rows < m; pad rows stay 0), then one GEMM launch per row step
-    launch_gemm(m, K, pl.nlive, mk(base, nullptr, 0, mpK, K), mk(F, pl.d_lo, 0, mK, K), 1.0, {}, st);
-    for (int64_t j = 0; j < pl.cap; ++j) {
-      const auto& s = pl.steps1[j];
-      if (s.cnt == 0) break;
-      if (j == 0)
-        launch_gemm(m, K, s.cnt, mk(X, pl.d_lo, 1, mK, K), none(), 0.0,
-                    {term(mk(pool, pl.d_slot0, pl.off_Dinv, blk, mp), mk(F, pl.d_lo, 1, mK, K), m)}, st);
-      else
-        launch_gemm(m, K, s.cnt, mk(X, pl.d_lo, 1 + j, mK, K), none(), 0.0,
-                    {term(mk(pool, pl.d_slot0, pl.off_Dinv + j, blk, mp), mk(F, pl.d_lo, 1 + j, mK, K), m),
-                     term(mk(pool, pl.d_slot0, pl.off_AD + j, blk, mp), mk(X, pl.d_lo, j, mK, K), m)},
-                    st);
-      launch_gemm(mp, K, s.cnt, mk(base, nullptr, 0, mpK, K), mk(base, nullptr, 0, mpK, K), 1.0,
-                  {term(mk(pool, pl.d_slot0, pl.off_Tb + j, blk, mp), mk(X, pl.d_lo, 1 + j, mK, K), m)}, st);
-    }
-  }
-  pl.ev_mark(1, st);
-  // interface RHS (ref dichotomy.py:239-276): f~_q = base_q + Fc_{q-1} y_{q-1,last}
-  launch_gemm(mp, K, pl.ncarry, mk(base, pl.carry_q, 0, mpK, K), mk(base, pl.carry_q, 0, mpK, K), 1.0,
-              {term(mk(pool, pl.carry_fc, 0, blk, mp), mk(X, pl.carry_row, 0, mK, K), m)}, st);
-  // Algorithm 1: z_node = R_node f~[lo..hi]  (all nodes, one launch)
-  const int nn = (int)pl.nodes.size();
-  {
-    // k per node = size*mp == rld
-    launch_gemm(mp, K, nn, mk(z, nullptr, 0, mpK, K), none(), 0.0,
-                {term(mk(pl.Rrows.d(), pl.d_roff, 0, 1, 0, pl.d_rld), mk(base, pl.d_nlo, 0, mpK, K), 0, 1.0, pl.d_rld)},
-                st);
-  }
-  for (const auto& lev : pl.levels) {
+  launch_gemm(mp, K, pl.nz, mk(z, pl.z_id, 0, mpK, K), none(), 0.0,
+              {term(mk(pl.Rrows.d(), pl.z_roff, 0, 1, 0, pl.z_rld), mk(ft, pl.z_nlo, 0, mpK, K), 0, 1.0, pl.z_rld)}, st);
+  for (const auto& lev : pl.levels)
     launch_gemm(mp, K, lev.count, mk(xt, lev.c_idx, 0, mpK, K), mk(z, lev.z_idx, 0, mpK, K), 1.0,
                 {term(mk(pl.EH.d(), lev.e_idx, 0, blk, mp), mk(xt, lev.xl_idx, 0, mpK, K), mp),
                  term(mk(pl.EH.d(), lev.h_idx, 0, blk, mp), mk(xt, lev.xh_idx, 0, mpK, K), mp)},
                 st);
-  }
-  pl.ev_mark(2, st);
+}
+
+// Backward sweeps of the owned ranges (x~ known), x[lo_q] = x~_q.
+void solve_backward(btd_plan& pl, const double* F, double* X, int64_t K, cudaStream_t st) {
+  const int64_t mp = pl.mp, m = pl.m, blk = pl.blk, mpK = mp * K, mK = m * K;
+  double* pool = pl.pool.d();
+  double* xt = pl.xt.d() + pl.q0 * mpK;
   if (pl.mode == 0) {
-    ChainArgs a;
-    a.lo = pl.d_lo; a.nint = pl.d_nint; a.slot0 = pl.d_slot0; a.nr = (int)nr;
-    a.m = (int)m; a.n = pl.n; a.K = K; a.F = F; a.X = X;
-    a.AD = pool + pl.off_AD * blk; a.Dinv = pool + pl.off_Dinv * blk; a.Tb = pool + pl.off_Tb * blk;
-    a.S = pool + pl.off_S * blk; a.G = pool + pl.off_G * blk;
-    a.base = base; a.xt = xt;
-    launch_chain(mp, a, false, st);
-  } else {
-    // x[lo_q] = x~_q
-    launch_gemm(m, K, pl.nlive, mk(X, pl.d_lo, 0, mK, K), mk(xt, nullptr, 0, mpK, K), 1.0, {}, st);
-    for (int64_t j = pl.cap - 1; j >= 0; --j) {
-      const auto& s = pl.steps1[j];
-      // x_j = y_j + G_j x~_q + S_j x_{j+1}   (x_{j+1} an interior row)
-      launch_gemm(m, K, s.nx, mk(X, s.x_row, 0, mK, K), mk(X, s.x_row, 0, mK, K), 1.0,
-                  {term(mk(pool, s.x_slot, pl.off_G, blk, mp), mk(xt, s.x_q, 0, mpK, K), mp),
-                   term(mk(pool, s.x_slot, pl.off_S, blk, mp), mk(X, s.x_row, 1, mK, K), m)},
-                  st);
-      // last interior row: x_{j+1} = x~_{q+1}
-      launch_gemm(m, K, s.nt, mk(X, s.t_row, 0, mK, K), mk(X, s.t_row, 0, mK, K), 1.0,
-                  {term(mk(pool, s.t_slot, pl.off_G, blk, mp), mk(xt, s.t_q, 0, mpK, K), mp),
-                   term(mk(pool, s.t_slot, pl.off_S, blk, mp), mk(xt, s.t_q, 1, mpK, K), mp)},
-                  st);
-    }
+    launch_chain(mp, chain_args(pl, F, X, K, nullptr, 0), false, st);
+    return;
   }
-  pl.ev_mark(3, st);
+  launch_gemm(m, K, pl.nlive, mk(X, pl.d_lo, 0, mK, K), mk(xt, nullptr, 0, mpK, K), 1.0, {}, st);
+  for (int64_t j = pl.cap - 1; j >= 0; --j) {
+    const auto& s = pl.steps1[j];
+    // x_j = y_j + G_j x~_q + S_j x_{j+1}   (x_{j+1} an interior row)
+    launch_gemm(m, K, s.nx, mk(X, s.x_row, 0, mK, K), mk(X, s.x_row, 0, mK, K), 1.0,
+                {term(mk(pool, s.x_slot, pl.off_G, blk, mp), mk(xt, s.x_q, 0, mpK, K), mp),
+                 term(mk(pool, s.x_slot, pl.off_S, blk, mp), mk(X, s.x_row, 1, mK, K), m)},
+                st);
+    // last interior row: x_{j+1} = x~_{q+1}
+    launch_gemm(m, K, s.nt, mk(X, s.t_row, 0, mK, K), mk(X, s.t_row, 0, mK, K), 1.0,
+                {term(mk(pool, s.t_slot, pl.off_G, blk, mp), mk(xt, s.t_q, 0, mpK, K), mp),
+                 term(mk(pool, s.t_slot, pl.off_S, blk, mp), mk(xt, s.t_q, 1, mpK, K), mp)},
+                st);
+  }
+}
+
+// Single-device solve: forward -> interface RHS -> tree -> backward.
+void solve_device(btd_plan& pl, const double* F, double* X, int64_t K, cudaStream_t st) {
+  const int64_t mp = pl.mp, m = pl.m, blk = pl.blk, mpK = mp * K, mK = m * K;
+  double* ft = pl.ft.d();
+  pl.ev_mark(st);
+  solve_forward(pl, F, X, K, ft, mpK, st);
+  pl.ev_mark(st);
+  // f~_{q+1} += Fc_q y_{q,last}   (ref dichotomy.py:239-276)
+  launch_gemm(mp, K, pl.ncarry, mk(ft, pl.carry_src, 1, mpK, K), mk(ft, pl.carry_src, 1, mpK, K), 1.0,
+              {term(mk(pl.pool.d(), pl.carry_fc, 0, blk, mp), mk(X, pl.carry_row, 0, mK, K), m)}, st);
+  solve_tree(pl, K, st);
+  pl.ev_mark(st);
+  solve_backward(pl, F, X, K, st);
+  pl.ev_mark(st);
+}
+
+// Sharded phase A: local sweeps, then this rank's (base, carry) pairs into exch [nrl][2][mp][K].
+void solve_shard_a(btd_plan& pl, const double* F, double* X, int64_t K, double* exch, cudaStream_t st) {
+  const int64_t mp = pl.mp, m = pl.m, blk = pl.blk, mpK = mp * K, mK = m * K;
+  CK(cudaMemsetAsync(exch, 0, (size_t)pl.nrl * 2 * mpK * sizeof(double), st));
+  pl.ev_mark(st);
+  solve_forward(pl, F, X, K, exch, 2 * mpK, st);
+  pl.ev_mark(st);
+  launch_gemm(mp, K, pl.ncarry, mk(exch + mpK, pl.carry_src, 0, 2 * mpK, K), none(), 0.0,
+              {term(mk(pl.pool.d(), pl.carry_fc, 0, blk, mp), mk(X, pl.carry_row, 0, mK, K), m)}, st);
+}
+
+// Sharded phase B: interface RHS from the all-gathered pairs, tree, local recovery.
+void solve_shard_b(btd_plan& pl, const double* exch_all, const double* F, double* X, int64_t K, cudaStream_t st) {
+  const int64_t mpK = pl.mp * K;
+  assemble_ft_kernel<<<592, 256, 0, st>>>(exch_all, pl.ft.d(), pl.nr, mpK);
+  CK_LAUNCH();
+  solve_tree(pl, K, st);
+  pl.ev_mark(st);
+  solve_backward(pl, F, X, K, st);
+  pl.ev_mark(st);
+}
+
+int guarded(btd_plan* pl, void* stream, const std::function<void(cudaStream_t)>& fn) {
+  g_err.clear();
+  if (!pl) { g_err = "NULL plan"; return BTD_ERR_INVALID_ARG; }
+  try {
+    DeviceGuard dg(pl->device);
+    std::lock_guard<std::mutex> lk(pl->mu);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (pl->last_stream != st && pl->scratch_k) CK(cudaStreamSynchronize(pl->last_stream));
+    pl->last_stream = st;
+    fn(st);
+  } catch (const BtdError& e) {
+    return e.code;
+  }
+  return BTD_OK;
+}
+
+int create_impl(const double* diag, const double* lower, const double* upper, int64_t n, int64_t m, int64_t ranks,
+                int64_t split, int rank, int world, int device, int flags, void* stream, btd_plan** out_plan,
+                int64_t* err_info) {
+  g_err.clear();
+  if (err_info) { err_info[0] = -1; err_info[1] = -1; }
+  if (!out_plan) { g_err = "out_plan is NULL"; return BTD_ERR_INVALID_ARG; }
+  *out_plan = nullptr;
+  if (n < 1 || m < 1) { g_err = "need n >= 1 and m >= 1"; return BTD_ERR_DIMENSION; }
+  if (ranks < 1 || ranks > n) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "ranks=%lld outside [1, N=%lld]", (long long)ranks, (long long)n);
+    g_err = buf;
+    return BTD_ERR_INVALID_RANKS;  // ref dichotomy.py:326-327
+  }
+  if (world < 1 || rank < 0 || rank >= world) { g_err = "bad rank/world"; return BTD_ERR_INVALID_ARG; }
+  if (!diag || (n > 1 && (!lower || !upper))) { g_err = "NULL matrix pointer"; return BTD_ERR_INVALID_ARG; }
+  auto* pl = new btd_plan();
+  pl->device = device;
+  pl->n = n; pl->m = m; pl->ranks = ranks; pl->split = std::max<int64_t>(1, split);
+  pl->rank = rank; pl->world = world;
+  int64_t row = -1, rng = -1;
+  try {
+    DeviceGuard dg(device);
+    cudaStream_t st = (cudaStream_t)stream;
+    build_local(*pl, diag, lower, upper, flags, st, &row, &rng);
+    if (world == 1) build_finish(*pl, pl->contrib.d(), st, &row);
+  } catch (const BtdError& e) {
+    if (err_info) { err_info[0] = row; err_info[1] = rng; }
+    delete pl;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    delete pl;
+    return BTD_ERR_CUDA;
+  }
+  *out_plan = pl;
+  return BTD_OK;
 }
 
 }  // namespace
@@ -915,66 +1077,82 @@ const char* btd_last_error(void) { return g_err.c_str(); }
 int btd_plan_create(const double* diag, const double* lower, const double* upper, int64_t n, int64_t m,
                     int64_t ranks, int64_t split, int device, int flags, void* stream, btd_plan** out_plan,
                     int64_t* err_row) {
-  g_err.clear();
+  int64_t info[2] = {-1, -1};
+  const int rc = create_impl(diag, lower, upper, n, m, ranks, split, 0, 1, device, flags, stream, out_plan, info);
+  if (err_row) *err_row = info[0];
+  return rc;
+}
+
+int btd_plan_create_shard(const double* diag, const double* lower, const double* upper, int64_t n, int64_t m,
+                          int64_t ranks, int64_t split, int rank, int world, int device, int flags, void* stream,
+                          btd_plan** out_plan, int64_t* err_info) {
+  return create_impl(diag, lower, upper, n, m, ranks, split, rank, world, device, flags, stream, out_plan, err_info);
+}
+
+int btd_shard_contrib(btd_plan* pl, double* dst, int64_t* nelems, void* stream) {
+  if (!pl || !nelems) return BTD_ERR_INVALID_ARG;
+  *nelems = pl->nrl * 4 * pl->blk;
+  if (!dst) return BTD_OK;
+  return guarded(pl, stream, [&](cudaStream_t st) {
+    CK(cudaMemcpyAsync(dst, pl->contrib.p, (size_t)(*nelems) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  });
+}
+
+int btd_shard_finish(btd_plan* pl, const double* contrib_all, void* stream, int64_t* err_row) {
   if (err_row) *err_row = -1;
-  if (!out_plan) { g_err = "out_plan is NULL"; return BTD_ERR_INVALID_ARG; }
-  *out_plan = nullptr;
-  if (n < 1 || m < 1) { g_err = "need n >= 1 and m >= 1"; return BTD_ERR_DIMENSION; }
-  if (ranks < 1 || ranks > n) {
-    char buf[128];
-    snprintf(buf, sizeof buf, "ranks=%lld outside [1, N=%lld]", (long long)ranks, (long long)n);
-    g_err = buf;
-    return BTD_ERR_INVALID_RANKS;  // ref dichotomy.py:326-327
-  }
-  if (!diag || (n > 1 && (!lower || !upper))) { g_err = "NULL matrix pointer"; return BTD_ERR_INVALID_ARG; }
-  auto* pl = new btd_plan();
-  pl->device = device;
-  pl->n = n; pl->m = m; pl->ranks = ranks; pl->split = std::max<int64_t>(1, split);
+  if (!pl || !contrib_all) return BTD_ERR_INVALID_ARG;
+  if (pl->finished) return BTD_OK;
   int64_t row = -1;
-  try {
-    DeviceGuard dg(device);
-    build_plan(*pl, diag, lower, upper, flags, (cudaStream_t)stream, &row);
-  } catch (const BtdError& e) {
-    if (err_row) *err_row = row;
-    delete pl;
-    return e.code;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    delete pl;
-    return BTD_ERR_CUDA;
-  }
-  *out_plan = pl;
+  const int rc = guarded(pl, stream, [&](cudaStream_t st) { build_finish(*pl, contrib_all, st, &row); });
+  if (err_row) *err_row = row;
+  return rc;
+}
+
+int btd_shard_exchange_size(const btd_plan* pl, int64_t k, int64_t* nelems_local) {
+  if (!pl || !nelems_local) return BTD_ERR_INVALID_ARG;
+  *nelems_local = pl->nrl * 2 * pl->mp * k;
   return BTD_OK;
+}
+
+int btd_shard_solve_a(btd_plan* pl, const double* f_local, double* x_local, int64_t k, double* exch_local,
+                      void* stream) {
+  if (!pl || !pl->finished || (pl->nloc > 0 && (!f_local || !x_local)) || !exch_local || k < 1) {
+    g_err = "btd_shard_solve_a: bad argument or unfinished plan";
+    return BTD_ERR_INVALID_ARG;
+  }
+  return guarded(pl, stream, [&](cudaStream_t st) {
+    ensure_scratch(*pl, k);
+    solve_shard_a(*pl, f_local, x_local, k, exch_local, st);
+  });
+}
+
+int btd_shard_solve_b(btd_plan* pl, const double* exch_all, const double* f_local, double* x_local, int64_t k,
+                      void* stream) {
+  if (!pl || !pl->finished || !exch_all || (pl->nloc > 0 && !x_local) || k < 1) {
+    g_err = "btd_shard_solve_b: bad argument or unfinished plan";
+    return BTD_ERR_INVALID_ARG;
+  }
+  return guarded(pl, stream, [&](cudaStream_t st) {
+    ensure_scratch(*pl, k);
+    solve_shard_b(*pl, exch_all, f_local, x_local, k, st);
+  });
 }
 
 int btd_plan_solve(btd_plan* pl, const double* f, double* x, int64_t k, void* stream) {
-  g_err.clear();
   if (!pl || !f || !x) { g_err = "NULL argument"; return BTD_ERR_INVALID_ARG; }
   if (k < 1) { g_err = "k must be >= 1"; return BTD_ERR_DIMENSION; }
-  try {
-    DeviceGuard dg(pl->device);
-    std::lock_guard<std::mutex> lk(pl->mu);
-    cudaStream_t st = (cudaStream_t)stream;
-    if (pl->last_stream != st && pl->scratch_k) CK(cudaStreamSynchronize(pl->last_stream));
-    pl->last_stream = st;
+  if (pl->world != 1) { g_err = "sharded plan: use btd_shard_solve_a/b"; return BTD_ERR_INVALID_ARG; }
+  return guarded(pl, stream, [&](cudaStream_t st) {
     ensure_scratch(*pl, k);
     solve_device(*pl, f, x, k, st);
-  } catch (const BtdError& e) {
-    return e.code;
-  }
-  return BTD_OK;
+  });
 }
 
 int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int64_t k, void* stream) {
-  g_err.clear();
   if (!pl || !f_host || !x_host) { g_err = "NULL argument"; return BTD_ERR_INVALID_ARG; }
   if (k < 1) { g_err = "k must be >= 1"; return BTD_ERR_DIMENSION; }
-  try {
-    DeviceGuard dg(pl->device);
-    std::lock_guard<std::mutex> lk(pl->mu);
-    cudaStream_t st = (cudaStream_t)stream;
-    if (pl->last_stream != st && pl->scratch_k) CK(cudaStreamSynchronize(pl->last_stream));
-    pl->last_stream = st;
+  if (pl->world != 1) { g_err = "sharded plan: use btd_shard_solve_a/b"; return BTD_ERR_INVALID_ARG; }
+  return guarded(pl, stream, [&](cudaStream_t st) {
     const size_t bytes = (size_t)pl->n * pl->m * k * sizeof(double);
     if (pl->hostio_k != k) {
       pl->hostio.alloc(bytes);
@@ -985,22 +1163,17 @@ int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int6
     solve_device(*pl, pl->hostio.d(), pl->hostio.d(), k, st);
     CK(cudaMemcpyAsync(x_host, pl->hostio.p, bytes, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-  } catch (const BtdError& e) {
-    return e.code;
-  }
-  return BTD_OK;
+  });
 }
 
 int btd_plan_destroy(btd_plan* pl) {
   if (!pl) return BTD_OK;
-  {
-    int prev = -1;
-    cudaGetDevice(&prev);
-    cudaSetDevice(pl->device);
-    cudaDeviceSynchronize();
-    delete pl;
-    if (prev >= 0) cudaSetDevice(prev);
-  }
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(pl->device);
+  cudaDeviceSynchronize();
+  delete pl;
+  if (prev >= 0) cudaSetDevice(prev);
   return BTD_OK;
 }
 
@@ -1034,8 +1207,10 @@ int btd_plan_query(const btd_plan* pl, btd_plan_info* info) {
   memset(info, 0, sizeof *info);
   info->n = pl->n; info->m = pl->m; info->mp = pl->mp; info->ranks = pl->ranks; info->split = pl->split;
   info->nranges = pl->nr; info->L = pl->L; info->tree_nodes = (int64_t)pl->nodes.size();
-  info->tree_depth = pl->depth; info->factor_bytes = pl->factor_bytes; info->row_lo = 0; info->row_hi = pl->n;
+  info->tree_depth = pl->depth; info->factor_bytes = pl->factor_bytes;
+  info->row_lo = pl->R0; info->row_hi = pl->R0 + pl->nloc;
   info->device = pl->device; info->mode = pl->mode;
+  info->rank = pl->rank; info->world = pl->world; info->range_lo = pl->q0; info->range_hi = pl->q1;
   return BTD_OK;
 }
 

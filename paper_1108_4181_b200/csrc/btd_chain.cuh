@@ -36,8 +36,9 @@ struct ChainArgs {
   const double* Tb;
   const double* S;
   const double* G;
-  double* base;          // fwd out: [nr][MP][K]
-  const double* xt;      // bwd in:  [nr+1][MP][K]
+  double* base;          // fwd out: range q at base + q*base_stride ([MP][K] each)
+  int64_t base_stride;
+  const double* xt;      // bwd in:  [nr+1][MP][K], range q uses blocks q and q+1
 };
 
 // acc += A(warp rows, MP cols, global) @ Bs(MP x cols, smem, ld LDB)
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(32 * WR * WC) chain_fwd_kernel(ChainArgs a) {
   else
     zero_acc(ser);
   if (nint <= 0) {
-    store_tile(ser, a.base + (int64_t)q * MP * K, K, r0, c0 + cw0, MP, g, t, vec);
+    store_tile(ser, a.base + (int64_t)q * a.base_stride, K, r0, c0 + cw0, MP, g, t, vec);
     return;
   }
   cp_tile<MP, KT, LD, NT>(Fs0, a.F + (lo + 1) * rowK, K, c0, a.m, vec);
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(32 * WR * WC) chain_fwd_kernel(ChainArgs a) {
     __syncthreads();
   }
   wgemm<MP, TM, TN, 2>(ser, a.Tb + (slot0 + nint - 1) * blk + r0 * MP, Ys + cw0, LD, g, t);
-  store_tile(ser, a.base + (int64_t)q * MP * K, K, r0, c0 + cw0, MP, g, t, vec);
+  store_tile(ser, a.base + (int64_t)q * a.base_stride, K, r0, c0 + cw0, MP, g, t, vec);
 }
 
 // Backward sweep: per row j (descending) two segments through one ring:

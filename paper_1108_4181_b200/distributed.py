@@ -1,0 +1,195 @@
+"""Row-sharded dichotomy solve across GPUs (one process per GPU, NCCL).
+
+The reference runs Algorithm 2 on *virtual* ranks inside one process
+(``harness.py:147-216``): every rank sweeps its own range, the per-range
+interface pairs (base, carry) are all-gathered in ceil(log2 p) dissemination
+rounds, every rank solves the reduced system and recovers its range.  Here
+the ranks are real processes, one B200 each:
+
+* plan: each rank factors only its ranges (its block rows of the matrix) and
+  emits four reduced-system contributions per range; one NCCL all-gather of
+  those (4 M^2 doubles per range; the paper's step 1.2) lets every rank
+  assemble the reduced system and its partition-tree inverse rows;
+* solve: phase A (local fused sweeps) -> one NCCL all-gather of the (base,
+  carry) pairs (2 M K doubles per range, the reference's exchange) ->
+  phase B (interface RHS, tree solve, local recovery).
+
+On NVSwitch a single all-gather replaces the dissemination rounds; the stage
+law (ceil(log2 p) logical stages) is reported by :func:`stage_count`.
+The local compute is the C ABI of include/blocktri_b200.h; a ``backend``
+object can replace it (the CPU gloo tests plug in a numpy restatement to
+exercise this orchestration without a GPU).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _native
+from . import errors as _err
+
+BIG = 1 << 62
+
+
+def stage_count(p: int) -> int:
+    """Logical dissemination stages of the interface exchange (ref harness.py:153, 280-283)."""
+    return 0 if p <= 1 else math.ceil(math.log2(p))
+
+
+class NativeBackend:
+    """Local compute through the sm_100a library (CUDA tensors)."""
+
+    def __init__(self, device):
+        import torch
+
+        self.torch = torch
+        self.device = device
+        self.lib = _native.load()
+        self.comm_device = f"cuda:{device}"
+
+    def _stream(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    @staticmethod
+    def _p(t):
+        return ctypes.c_void_p(t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data)
+
+    def create(self, diag, lower, upper, n, m, ranks, split, rank, world):
+        torch = self.torch
+        flags = 0
+        if isinstance(diag, torch.Tensor):
+            flags = _native.BTD_MATRIX_ON_DEVICE
+            arrs = [a.to(device=f"cuda:{self.device}", dtype=torch.float64).contiguous() for a in (diag, lower, upper)]
+        else:
+            arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (diag, lower, upper)]
+        h = ctypes.c_void_p()
+        info = (ctypes.c_int64 * 2)(-1, -1)
+        with torch.cuda.device(self.device):
+            st = self.lib.btd_plan_create_shard(self._p(arrs[0]), self._p(arrs[1]), self._p(arrs[2]), n, m, ranks,
+                                                split, rank, world, self.device, flags, self._stream(),
+                                                ctypes.byref(h), info)
+        return h, st, int(info[0]), int(info[1])
+
+    def info(self, h):
+        pi = _native.PlanInfo()
+        _native.check(self.lib.btd_plan_query(h, ctypes.byref(pi)))
+        return pi
+
+    def contrib(self, h):
+        torch = self.torch
+        nel = ctypes.c_int64()
+        _native.check(self.lib.btd_shard_contrib(h, None, ctypes.byref(nel), None))
+        buf = torch.empty(nel.value, dtype=torch.float64, device=f"cuda:{self.device}")
+        with torch.cuda.device(self.device):
+            _native.check(self.lib.btd_shard_contrib(h, self._p(buf), ctypes.byref(nel), self._stream()))
+        return buf
+
+    def finish(self, h, contrib_all):
+        row = ctypes.c_int64(-1)
+        with self.torch.cuda.device(self.device):
+            st = self.lib.btd_shard_finish(h, self._p(contrib_all), self._stream(), ctypes.byref(row))
+        return st, row.value
+
+    def empty(self, nel):
+        return self.torch.empty(nel, dtype=self.torch.float64, device=f"cuda:{self.device}")
+
+    def exchange_size(self, h, k):
+        nel = ctypes.c_int64()
+        _native.check(self.lib.btd_shard_exchange_size(h, k, ctypes.byref(nel)))
+        return nel.value
+
+    def solve_a(self, h, f_local, x_local, k, exch):
+        with self.torch.cuda.device(self.device):
+            _native.check(self.lib.btd_shard_solve_a(h, self._p(f_local), self._p(x_local), k, self._p(exch),
+                                                     self._stream()))
+
+    def solve_b(self, h, exch_all, f_local, x_local, k):
+        with self.torch.cuda.device(self.device):
+            _native.check(self.lib.btd_shard_solve_b(h, self._p(exch_all), self._p(f_local), self._p(x_local), k,
+                                                     self._stream()))
+
+    def destroy(self, h):
+        self.lib.btd_plan_destroy(h)
+
+
+class ShardedPlan:
+    """One rank's share of a row-sharded plan (mirrors ref DichotomyPlan +
+    the per-rank state of ref harness.DichotomyRankProgram)."""
+
+    def __init__(self, diag, lower, upper, ranks, *, split=1, group=None, device=None, backend=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        n, m = int(diag.shape[0]), int(diag.shape[1])
+        if ranks < 1 or ranks > n:
+            raise _err.InvalidRankCount(f"ranks={ranks} outside [1, N={n}]")
+        if backend is None:
+            import torch
+
+            backend = NativeBackend(torch.cuda.current_device() if device is None else device)
+        self.be = backend
+        self.n, self.m, self.ranks, self.split = n, m, int(ranks), int(split)
+        h, st, row, rng = backend.create(diag, lower, upper, n, m, self.ranks, self.split, self.rank, self.world)
+        # every rank raises the same error: the first failing range wins (ref loop order)
+        try:
+            self._raise_consistently(st, row, rng)
+        except _err.BlocktriError:
+            if st == 0:
+                backend.destroy(h)
+            raise
+        self.h = h
+        local = backend.contrib(h)
+        allc = backend.empty(local.numel() * self.world)
+        dist.all_gather_into_tensor(allc, local, group=group)
+        st, row = backend.finish(h, allc)
+        if st:
+            msg = _native.last_error() if isinstance(backend, NativeBackend) else "singular reduced system"
+            if st == _native.BTD_ERR_SINGULAR_PIVOT:
+                raise _err.SingularPivot(row, msg)
+            _native.check(st, row)
+        info = backend.info(h)
+        self.row_lo, self.row_hi = int(info.row_lo), int(info.row_hi)
+        self.nranges, self.L = int(info.nranges), int(info.L)
+        self.range_lo, self.range_hi = int(info.range_lo), int(info.range_hi)
+
+    def _raise_consistently(self, st, row, rng):
+        import torch
+
+        code = torch.tensor([st, row, rng if st else BIG], dtype=torch.int64, device=self.be.comm_device)
+        allc = torch.empty(3 * self.world, dtype=torch.int64, device=self.be.comm_device)
+        self.dist.all_gather_into_tensor(allc, code, group=self.group)
+        c = allc.view(self.world, 3).cpu().numpy()
+        bad = [r for r in range(self.world) if c[r, 0] != 0]
+        if not bad:
+            return
+        first = min(bad, key=lambda r: (c[r, 0] != _native.BTD_ERR_SINGULAR_PIVOT, c[r, 2]))
+        code0, row0 = int(c[first, 0]), int(c[first, 1])
+        if code0 == _native.BTD_ERR_SINGULAR_PIVOT:
+            raise _err.SingularPivot(row0, f"block row {row0}: singular pivot (range {int(c[first, 2])})")
+        if code0 == _native.BTD_ERR_INVALID_RANKS:
+            raise _err.InvalidRankCount("invalid rank count")
+        raise _err.DeviceError(f"shard plan build failed on rank {first} with status {code0}")
+
+    def solve(self, f_local, out=None):
+        """f_local: (row_hi - row_lo, m, K) rows of this shard -> x_local
+        (written into ``out`` when given; may alias f_local)."""
+        k = int(f_local.shape[2])
+        x_local = f_local.new_empty(f_local.shape) if out is None else out
+        nel = self.be.exchange_size(self.h, k)
+        exch = self.be.empty(nel)
+        self.be.solve_a(self.h, f_local, x_local, k, exch)
+        allx = self.be.empty(nel * self.world)
+        self.dist.all_gather_into_tensor(allx, exch, group=self.group)
+        self.be.solve_b(self.h, allx, f_local, x_local, k)
+        return x_local
+
+    def close(self):
+        if getattr(self, "h", None) is not None:
+            self.be.destroy(self.h)
+            self.h = None

@@ -1,0 +1,102 @@
+"""Native row-sharded path on one GPU.
+
+World sizes 2 and 4 are emulated in one process: every shard's phases run
+one after another and the all-gathers are host-side concatenations of the
+shards' device buffers (no kernel waits on another).  ShardedPlan is also run
+over a real single-rank NCCL process group."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import blocktri_oracle as O
+from golden_cases import singular_inputs
+from paper_1108_4181_b200 import configs, errors
+from paper_1108_4181_b200.distributed import NativeBackend, ShardedPlan
+
+pytestmark = pytest.mark.gpu
+
+
+def _emulate(d, lo, up, f, ranks, split, world):
+    import torch
+
+    be = NativeBackend(0)
+    hs, infos = [], []
+    for r in range(world):
+        h, st, row, rng = be.create(d, lo, up, d.shape[0], d.shape[1], ranks, split, r, world)
+        if st:
+            for h_ in hs:
+                be.destroy(h_)
+            return ("error", st, row, rng)
+        hs.append(h)
+    allc = torch.cat([be.contrib(h) for h in hs])
+    for h in hs:
+        st, row = be.finish(h, allc)
+        assert st == 0
+    infos = [be.info(h) for h in hs]
+    k = f.shape[2]
+    ft = torch.from_numpy(f).cuda()
+    xs, exs = [], []
+    for h, inf in zip(hs, infos):
+        fl = ft[inf.row_lo:inf.row_hi].contiguous()
+        xl = torch.empty_like(fl)
+        ex = be.empty(be.exchange_size(h, k))
+        be.solve_a(h, fl, xl, k, ex)
+        xs.append((fl, xl))
+        exs.append(ex)
+    allx = torch.cat(exs)
+    for h, (fl, xl) in zip(hs, xs):
+        be.solve_b(h, allx, fl, xl, k)
+    torch.cuda.synchronize()
+    x = torch.cat([xl for _, xl in xs]).cpu().numpy()
+    for h in hs:
+        be.destroy(h)
+    return ("ok", x)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("n,m,k,ranks,split", [(256, 16, 8, 8, 1), (203, 8, 5, 4, 3), (96, 64, 4, 4, 2),
+                                               (64, 256, 4, 4, 1), (12, 3, 2, 8, 1)])
+def test_emulated_shards_match_oracle(world, n, m, k, ranks, split):
+    if (min(n, ranks * split)) % world:
+        pytest.skip("ranges not divisible by world")
+    d, lo, up, f = configs.dominant_numpy(n, m, k, seed=n + world)
+    res = _emulate(d, lo, up, f, ranks, split, world)
+    assert res[0] == "ok"
+    ref = O.plan_solve(O.plan_build(d, lo, up, ranks), f)
+    assert O.max_rel_err(res[1], ref) <= 1e-9
+    assert O.rel_residual(d, lo, up, res[1], f) <= 1e-10
+
+
+def test_emulated_shard_singular_reports_first_range():
+    d, lo, up = singular_inputs(24, 3, 19)
+    res = _emulate(d, lo, up, np.zeros((24, 3, 1)), 4, 1, 2)
+    # rank 0 is fine, rank 1 (ranges 2,3) fails at range 3 (rows 18..23), local row 0
+    assert res[0] == "error" and res[1] == 2 and res[3] == 3 and res[2] == 0
+    with pytest.raises(errors.SingularPivot) as info:
+        import blocktri_oracle as O2
+        O2.plan_build(d, lo, up, 4)
+    assert info.value.row == res[2]
+
+
+def test_sharded_plan_over_nccl_world1():
+    import torch
+    import torch.distributed as dist
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        d, lo, up, f = configs.dominant_numpy(512, 16, 16, seed=9)
+        plan = ShardedPlan(torch.from_numpy(d).cuda(), torch.from_numpy(lo).cuda(), torch.from_numpy(up).cuda(), 8,
+                           split=2)
+        x = plan.solve(torch.from_numpy(f).cuda()).cpu().numpy()
+        plan.close()
+    finally:
+        dist.destroy_process_group()
+    ref = O.plan_solve(O.plan_build(d, lo, up, 8), f)
+    assert O.max_rel_err(x, ref) <= 1e-9
