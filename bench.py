@@ -50,6 +50,9 @@ BENCH_CFG = {
     "c0": dict(subdomains_per_gpu=lambda w: 4, ranges_per_gpu=4),
     "c1": dict(subdomains_per_gpu=lambda w: 18, ranges_per_gpu=18),
     "c2": dict(subdomains_per_gpu=lambda w: 9, ranges_per_gpu=9),
+    # c3: the explicit interface Schur complement S (N=63, M=2048) of the 64-subdomain
+    # Helmholtz DD; P = 8 ranges of 8 interface rows (a multiple of 1/2/4/8 GPUs)
+    "c3": dict(subdomains_per_gpu=lambda w: 8 // w, ranges_per_gpu=8),
     "c4": dict(subdomains_per_gpu=lambda w: 8 * w, ranges_per_gpu=592),
 }
 
@@ -68,6 +71,7 @@ CPU_SAMPLE = {
     "c0": (512, 32, 4),
     "c1": (256, 256, 8),
     "c2": (512, 1024, 8),
+    "c3": (63, 16, 8),   # S of the same DD at nx = 512 (M = 512): flop-scaled to M = 2048
     "c4": (65536, 64, 16),
 }
 
@@ -188,23 +192,34 @@ class CpuSample:
         cfg = configs.CONFIGS[name]
         self.cfg = cfg
         ns, ks, ps = CPU_SAMPLE[name]
+        scale = 1.0
         if cfg["kind"] == "strip":
             d, lo, up, f = configs.strip_numpy(ns, cfg["m"], ks, cfg["shift"], 0)
+        elif cfg["kind"] == "schur":
+            from paper_1108_4181_b200 import schur
+
+            mx = 512
+            d, lo, up = schur.schur_blocks_numpy(mx, cfg["nz"] // 4, cfg["nsub"])
+            f = np.random.default_rng(0).standard_normal((d.shape[0], mx, ks))
+            scale = (mx / cfg["m"]) ** 2  # solve flops scale with M^2 at fixed N, K
         else:
             d, lo, up, f = configs.dominant_numpy(ns, cfg["m"], ks, 0)
         self.f = f
+        self.scale = scale
         self.ns, self.ks, self.ps = ns, ks, ps
         self.plan = coracle.CPlan(d, lo, up, ps)
         self.cores = coracle.threads()
         self.sample = (f"C port of the reference plan_solve (oracle/blocktri_oracle.c; ref dichotomy.py:358-390, "
                        f"_kernels.pyx:173-194) on N={ns} of {cfg['n']} block rows, K={ks} of {cfg['k']} columns, "
-                       f"P={ps}, {self.cores} threads; RHS/s scaled by N_s/N (solve cost is linear in N)")
+                       f"P={ps}, {self.cores} threads; RHS/s scaled by N_s/N (solve cost is linear in N)"
+                       + ("; c3: S of the same 64-subdomain DD on a 512 x 2048 grid (M = 512), RHS/s "
+                          "scaled by (512/2048)^2 (solve flops ~ N M^2 K)" if cfg["kind"] == "schur" else ""))
 
     def step(self):
         t0 = time.perf_counter()
         self.plan.solve(self.f)
         t = time.perf_counter() - t0
-        return self.ks / t * self.ns / self.cfg["n"], t
+        return self.ks / t * self.ns / self.cfg["n"] * self.scale, t
 
 
 def cpu_sample_run(name, steps=1):
@@ -230,7 +245,7 @@ def run_reference(args):
         cs.step()
     res = [cs.step() for _ in range(args.steps)]
     ts = [r[1] for r in res]
-    value = cs.ks * args.steps / sum(ts) * cs.ns / cfg["n"]
+    value = cs.ks * args.steps / sum(ts) * cs.ns / cfg["n"] * cs.scale
     line = {
         "impl": "reference", "metric": "rhs_columns_per_second", "value": value, "unit": "RHS/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,

@@ -22,7 +22,7 @@ CONFIGS = {
     "c0": dict(n=512, m=8, k=32, ranks=4, kind="dominant"),
     "c1": dict(n=4096, m=256, k=256, ranks=32, kind="strip", shift=0.01),
     "c2": dict(n=16384, m=64, k=1024, ranks=64, kind="dominant"),
-    "c3": dict(n=63, m=2048, k=128, ranks=8, kind="schur"),
+    "c3": dict(n=63, m=2048, k=128, ranks=8, kind="schur", nx=2048, nz=8192, nsub=64),
     "c4": dict(n=1 << 20, m=16, k=64, ranks=8, kind="dominant"),
 }
 
@@ -93,4 +93,20 @@ def generate(name, *, device=None, seed=0, n=None, k=None):
     if cfg["kind"] == "strip":
         return (strip_numpy(n, m, k, cfg["shift"], seed) if device is None
                 else strip_torch(n, m, k, cfg["shift"], seed, device))
-    raise ValueError(f"config {name} is assembled by paper_1108_4181_b200.schur")
+    if cfg["kind"] == "schur":
+        from . import schur
+
+        if device is None:
+            d, lo, up = schur.schur_blocks_numpy(cfg["nx"], cfg["nz"], cfg["nsub"], seed=seed)
+            f = np.random.default_rng(seed).standard_normal((d.shape[0], m, k)) if k else None
+            return d, lo, up, f
+        import torch
+
+        d, lo, up = schur.schur_blocks_torch(cfg["nx"], cfg["nz"], cfg["nsub"], device=device, seed=seed)
+        f = None
+        if k:
+            g = torch.Generator(device=device)
+            g.manual_seed(seed)
+            f = torch.randn((d.shape[0], m, k), dtype=torch.float64, device=device, generator=g)
+        return d, lo, up, f
+    raise ValueError(f"unknown config kind {cfg['kind']}")

@@ -257,7 +257,7 @@ struct btd_plan {
   int nlive = 0;  // local ranges whose interface row is < n
   // scratch
   int64_t scratch_k = 0;
-  DevBuf ft, zbuf, xt, hostio;
+  DevBuf ft, zbuf, xt, hostio, fcopy;  // fcopy: mode-1 staging of F when it aliases X
   int64_t hostio_k = 0;
   std::mutex mu;
   cudaStream_t last_stream = nullptr;
@@ -910,9 +910,18 @@ void solve_forward(btd_plan& pl, const double* F, double* X, int64_t K, double* 
   const int64_t mp = pl.mp, m = pl.m, blk = pl.blk;
   const int64_t mK = m * K;
   double* pool = pl.pool.d();
-  if (pl.mode == 0) {
+  if (pl.mode == 0) {  // each CTA owns its (rows, columns): in-place F == X is safe
     launch_chain(mp, chain_args(pl, F, X, K, base, base_stride), true, st);
     return;
+  }
+  // mode 1: a step's GEMM reads all of F[g] as its reduction operand while other
+  // CTAs write X[g]; stage F when the caller solves in place.
+  const size_t fbytes = (size_t)pl.nloc * mK * sizeof(double);
+  const char *f0 = (const char*)F, *x0 = (const char*)X;
+  if (fbytes && f0 < x0 + fbytes && x0 < f0 + fbytes) {
+    if (pl.fcopy.bytes < fbytes) pl.fcopy.alloc(fbytes);
+    CK(cudaMemcpyAsync(pl.fcopy.p, F, fbytes, cudaMemcpyDeviceToDevice, st));
+    F = pl.fcopy.d();
   }
   // mode 1: base_q = F[lo_q] (rows < m; pad rows stay 0), then one GEMM launch per row step
   launch_gemm(m, K, pl.nlive, mk(base, nullptr, 0, base_stride, K), mk(F, pl.d_lo, 0, mK, K), 1.0, {}, st);

@@ -54,6 +54,15 @@ _BY_NAME = {
 }
 
 
+_ORIGINAL = dict(_BY_NAME)
+
+
+def restore() -> None:
+    """Undo :func:`rebind`."""
+    globals().update(_ORIGINAL)
+    _BY_NAME.update(_ORIGINAL)
+
+
 def rebind(module) -> None:
     """Use another module's same-named exception classes (e.g. blocktri.errors)."""
     g = globals()

@@ -137,3 +137,28 @@ def test_no_factorization_during_solve_launch_count():
     plan_solve(plan, f)
     per_solve = _native.launch_count() - c0
     assert per_solve == 3 + 1 + (plan.tree_depth + 1)  # fwd, carry, z, levels, bwd
+
+
+@pytest.mark.parametrize("nx,nz,nsub,ranks", [(256, 1024, 16, 4), (320, 512, 8, 3), (64, 512, 32, 8)])
+def test_config3_schur_solve_family(nx, nz, nsub, ranks):
+    """Config-3 family (Helmholtz DD interface Schur complement), scaled down:
+    GPU plan_solve on the explicit S vs the CPU oracle on the same S."""
+    from paper_1108_4181_b200 import schur
+
+    d, lo, up = schur.schur_blocks_numpy(nx, nz, nsub)
+    f = np.random.default_rng(nx).standard_normal((d.shape[0], nx, 8))
+    plan = plan_build(BlockTriMatrix(d, lo, up), ranks)
+    assert plan.mode == (1 if nx > 256 else 0)
+    x = plan_solve(plan, f)
+    ref = O.plan_solve(O.plan_build(d, lo, up, ranks), f)
+    _check(d, lo, up, x, f, ref)
+
+
+def test_config3_gpu_assembly_matches_numpy():
+    import torch
+    from paper_1108_4181_b200 import schur
+
+    d, lo, up = schur.schur_blocks_numpy(128, 1024, 16)
+    dt, lt, ut = schur.schur_blocks_torch(128, 1024, 16)
+    assert np.abs(dt.cpu().numpy() - d).max() <= 1e-13 * np.abs(d).max()
+    assert np.abs(ut.cpu().numpy() - up).max() <= 1e-13 * np.abs(d).max()
