@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp",
-           os.path.join(CSRC, "btd_api.cu")]
+           os.path.join(CSRC, "btd_api.cu"), "-lcusolver", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -34,6 +34,8 @@
 #include <string>
 #include <vector>
 
+#include <cusolverDn.h>
+
 #include "blocktri_b200.h"
 #include "btd_chain.cuh"
 #include "btd_gemm.cuh"
@@ -132,6 +134,61 @@ __global__ void assemble_rows_kernel(const double* Y, const int64_t* ynb0, const
     const int64_t a = le / (s * mp), rest = le % (s * mp);
     const int64_t i = rest / mp, c = rest % mp;
     R[roff[b] + a * s * mp + i * mp + c] = Y[(ynb0[b] + i) * (int64_t)mp * mp + c * mp + a];
+  }
+}
+
+// row-major D (mp x mp) -> col-major copy of D (i.e. row-major D^T)
+__global__ void transpose_one_kernel(const double* in, double* out, int mp) {
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int r = by + i, c = bx + threadIdx.x;
+    tile[i][threadIdx.x] = (r < mp && c < mp) ? in[(int64_t)r * mp + c] : 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int r = bx + i, c = by + threadIdx.x;
+    if (r < mp && c < mp) out[(int64_t)r * mp + c] = tile[threadIdx.x][i];
+  }
+}
+
+// Reference pivot test on an LU of D (ref _kernels.pyx:35-63): fail at the first
+// k < m with |U_kk| <= rcond * ||D[:m,:m]||_inf.  D row-major, LU col-major.
+__global__ void lu_pivot_check_kernel(const double* D, const double* LU, int m, int mp, double rcond, int step,
+                                      int32_t* fail_step, int32_t* fail_col, int64_t slot) {
+  __shared__ double red[32];
+  __shared__ int redk[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double mx = 0.0;
+  for (int r = warp; r < m; r += nw) {
+    double sum = 0.0;
+    for (int c = lane; c < m; c += 32) sum += fabs(D[(int64_t)r * mp + c]);
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    mx = fmax(mx, sum);
+  }
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t = fmax(t, red[w]);
+    red[0] = t * rcond;
+  }
+  __syncthreads();
+  const double tol = red[0];
+  __syncthreads();
+  int kmin = m;
+  for (int k = tid; k < m; k += blockDim.x)
+    if (!(fabs(LU[(int64_t)k * mp + k]) > tol)) kmin = min(kmin, k);
+  for (int o = 16; o; o >>= 1) kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+  if (lane == 0) redk[warp] = kmin;
+  __syncthreads();
+  if (tid == 0) {
+    int k = m;
+    for (int w = 0; w < nw; ++w) k = min(k, redk[w]);
+    if (k < m && fail_step[slot] < 0) {
+      fail_step[slot] = step;
+      fail_col[slot] = k;
+    }
   }
 }
 
@@ -262,6 +319,10 @@ struct btd_plan {
   std::mutex mu;
   cudaStream_t last_stream = nullptr;
   int64_t factor_bytes = 0;
+  // cuSOLVER for block orders above 256 (preprocessing only)
+  cusolverDnHandle_t solver = nullptr;
+  DevBuf sv_work, sv_ipiv, sv_info, sv_lu;
+  int sv_lwork = 0;
   // profiling: 4 events per solve (before fwd, after fwd, after tree, after bwd)
   bool profiling = false;
   std::vector<cudaEvent_t> ev_free, ev_pending;
@@ -293,6 +354,7 @@ struct btd_plan {
   ~btd_plan() {
     for (auto e : ev_pending) cudaEventDestroy(e);
     for (auto e : ev_free) cudaEventDestroy(e);
+    if (solver) cusolverDnDestroy(solver);
   }
   template <class T>
   const T* upload(const std::vector<T>& v) {
@@ -324,6 +386,52 @@ void launch_inv(btd_plan& pl, int nbatch, const double* in, const int64_t* idx_i
                 int32_t* fail_col, DevBuf& ws, cudaStream_t st, const int64_t* fail_map = nullptr) {
   if (nbatch <= 0) return;
   const int mp = (int)pl.mp;
+  if (mp > 256) {
+    // cuSOLVER route: getrf on D (col-major view of D^T), reference pivot test on
+    // diag(U), getrs(transpose) against I -> D^{-1} written row-major.
+    auto host_idx = [&](const int64_t* di) {
+      std::vector<int64_t> h(nbatch);
+      if (di) CK(cudaMemcpy(h.data(), di, sizeof(int64_t) * nbatch, cudaMemcpyDeviceToHost));
+      else for (int b = 0; b < nbatch; ++b) h[b] = b;
+      return h;
+    };
+    const std::vector<int64_t> hin = host_idx(idx_in), hout = host_idx(idx_out), hmap = host_idx(fail_map);
+    auto cs = [&](cusolverStatus_t e, const char* what) {
+      if (e != CUSOLVER_STATUS_SUCCESS) fail(BTD_ERR_CUDA, std::string("cuSOLVER failure: ") + what);
+    };
+    if (!pl.solver) cs(cusolverDnCreate(&pl.solver), "create");
+    cs(cusolverDnSetStream(pl.solver, st), "set stream");
+    const size_t bb = (size_t)mp * mp;
+    if (pl.sv_lu.bytes < bb * sizeof(double)) {
+      pl.sv_lu.alloc(bb * sizeof(double));
+      pl.sv_ipiv.alloc(sizeof(int) * mp);
+      pl.sv_info.alloc(sizeof(int));
+      int lw = 0;
+      cs(cusolverDnDgetrf_bufferSize(pl.solver, mp, mp, pl.sv_lu.d(), mp, &lw), "bufferSize");
+      pl.sv_lwork = lw;
+      pl.sv_work.alloc(sizeof(double) * std::max(lw, 1));
+    }
+    for (int b = 0; b < nbatch; ++b) {
+      const double* D = in + (hin[b] + add_in) * (int64_t)bb;
+      double* O = out + (hout[b] + add_out) * (int64_t)bb;
+      dim3 tg((mp + 31) / 32, (mp + 31) / 32);
+      transpose_one_kernel<<<tg, dim3(32, 8), 0, st>>>(D, pl.sv_lu.d(), mp);
+      CK_LAUNCH();
+      cs(cusolverDnDgetrf(pl.solver, mp, mp, pl.sv_lu.d(), mp, pl.sv_work.d(), static_cast<int*>(pl.sv_ipiv.p),
+                          static_cast<int*>(pl.sv_info.p)),
+         "getrf");
+      lu_pivot_check_kernel<<<1, 512, 0, st>>>(D, pl.sv_lu.d(), (int)pl.m, mp, 1e-13, step, fail_step, fail_col,
+                                               hmap[b]);
+      CK_LAUNCH();
+      set_identity_kernel<<<256, 256, 0, st>>>(O, mp);
+      CK_LAUNCH();
+      cs(cusolverDnDgetrs(pl.solver, CUBLAS_OP_T, mp, mp, pl.sv_lu.d(), mp, static_cast<const int*>(pl.sv_ipiv.p), O,
+                          mp, static_cast<int*>(pl.sv_info.p)),
+         "getrs");
+    }
+    (void)ws;
+    return;
+  }
   InvDesc d;
   d.in = in;
   d.idx_in = idx_in;

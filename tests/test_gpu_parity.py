@@ -162,3 +162,14 @@ def test_config3_gpu_assembly_matches_numpy():
     dt, lt, ut = schur.schur_blocks_torch(128, 1024, 16)
     assert np.abs(dt.cpu().numpy() - d).max() <= 1e-13 * np.abs(d).max()
     assert np.abs(ut.cpu().numpy() - up).max() <= 1e-13 * np.abs(d).max()
+
+
+@pytest.mark.parametrize("m", [300, 64])
+def test_singular_pivot_large_blocks(m):
+    """Same SingularPivot row for block orders on the cuSOLVER (m > 256) and
+    Gauss-Jordan inversion routes (golden case sing_r7 with larger blocks)."""
+    e = META["errors"]["sing_r7"]
+    d, lo, up = singular_inputs(e["n"], m, e["singular_row"])
+    with pytest.raises(errors.SingularPivot) as info:
+        plan_build(BlockTriMatrix(d, lo, up), e["ranks"])
+    assert info.value.row == e["row"]
