@@ -467,35 +467,50 @@ void launch_inv(btd_plan& pl, int nbatch, const double* in, const int64_t* idx_i
 }
 
 // ---------------------------------------------------------------- chain kernels
-template <int MP, int KT, int WR, int WC>
+template <int MP, int KT, int WR, int WC, int NF = -1, int NY = -1>
 void launch_chain_t(const ChainArgs& a, bool fwd, cudaStream_t st) {
-  using Cfg = ChainCfg<MP, KT, WR, WC>;
-  const size_t smem = (size_t)(fwd ? 3 : 2) * MP * Cfg::LD * sizeof(double);
+  using Cfg = ChainCfg<MP, KT, WR, WC, NF, NY>;
+  const size_t smem = (size_t)(fwd ? Cfg::FWD_BUFS : Cfg::BWD_BUFS) * MP * Cfg::LD * sizeof(double);
   const int64_t ntile = (a.K + KT - 1) / KT;
   dim3 grid((unsigned)ntile, (unsigned)a.nr);
   if (fwd) {
     if (smem > 48 * 1024)
-      CK(cudaFuncSetAttribute(chain_fwd_kernel<MP, KT, WR, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CK(cudaFuncSetAttribute(chain_fwd_kernel<MP, KT, WR, WC, NF, NY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)smem));
-    chain_fwd_kernel<MP, KT, WR, WC><<<grid, Cfg::NT, smem, st>>>(a);
+    chain_fwd_kernel<MP, KT, WR, WC, NF, NY><<<grid, Cfg::NT, smem, st>>>(a);
   } else {
     if (smem > 48 * 1024)
-      CK(cudaFuncSetAttribute(chain_bwd_kernel<MP, KT, WR, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CK(cudaFuncSetAttribute(chain_bwd_kernel<MP, KT, WR, WC, NF, NY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)smem));
-    chain_bwd_kernel<MP, KT, WR, WC><<<grid, Cfg::NT, smem, st>>>(a);
+    chain_bwd_kernel<MP, KT, WR, WC, NF, NY><<<grid, Cfg::NT, smem, st>>>(a);
   }
   CK_LAUNCH();
 }
 
+// Chain-kernel configuration per padded block order (MP, KT, warp rows x warp cols).
+// BTD_CHAIN_VARIANT selects alternatives for tuning experiments.
 void launch_chain(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
   if (a.nr <= 0) return;
+  static int variant = -1;
+  if (variant < 0) {
+    const char* e = getenv("BTD_CHAIN_VARIANT");
+    variant = e ? atoi(e) : 0;
+  }
   switch (mp) {
     case 8: launch_chain_t<8, 32, 1, 4>(a, fwd, st); break;
     case 16: launch_chain_t<16, 16, 1, 1>(a, fwd, st); break;
     case 32: launch_chain_t<32, 32, 2, 2>(a, fwd, st); break;
-    case 64: launch_chain_t<64, 64, 4, 2>(a, fwd, st); break;
-    case 128: launch_chain_t<128, 32, 8, 1>(a, fwd, st); break;
-    case 256: launch_chain_t<256, 32, 8, 1>(a, fwd, st); break;
+    case 64:
+      if (variant == 2) launch_chain_t<64, 64, 8, 2, 2, 0>(a, fwd, st);
+      else if (variant == 3) launch_chain_t<64, 64, 8, 2, 3, 0>(a, fwd, st);
+      else if (variant == 4) launch_chain_t<64, 64, 8, 2, 2, 3>(a, fwd, st);
+      else launch_chain_t<64, 64, 8, 2>(a, fwd, st);
+      break;
+    case 128: launch_chain_t<128, 32, 16, 1>(a, fwd, st); break;
+    case 256:
+      if (variant == 1) launch_chain_t<256, 32, 16, 1>(a, fwd, st);
+      else launch_chain_t<256, 16, 16, 1>(a, fwd, st);
+      break;
     default: fail(BTD_ERR_UNSUPPORTED, "no chain kernel for this block order");
   }
 }

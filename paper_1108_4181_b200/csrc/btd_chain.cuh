@@ -217,7 +217,7 @@ BTD_DEVINL void cp_tile(double* Ys, const double* __restrict__ P, int64_t K, int
   cp_async_commit();
 }
 
-template <int MP, int KT, int WR, int WC>
+template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1>
 struct ChainCfg {
   static constexpr int NW = WR * WC, NT = 32 * NW;
   static constexpr int RW = MP / WR, CW = KT / WC;
@@ -227,6 +227,12 @@ struct ChainCfg {
   // factor-fragment prefetch distance (pair steps), one group ahead
   static constexpr int PF = NS < 4 ? NS : (TM >= 4 ? 2 : 4);
   static constexpr int GPS = NS / PF;  // groups per segment
+  // cp.async ring depths: forward F tiles, backward y tiles (0 = register prefetch)
+  // (measured on B200: deeper rings hurt the 16x16 one-warp tiles of c4)
+  static constexpr int NF = NF_ >= 0 ? NF_ : (MP <= 16 ? 2 : (MP <= 64 ? 3 : 2));
+  static constexpr int NY = NY_ >= 0 ? NY_ : (MP <= 16 ? 0 : (MP <= 64 ? 3 : 0));
+  static constexpr int FWD_BUFS = 1 + NF;
+  static constexpr int BWD_BUFS = 2 + NY;
   static_assert(RW % 8 == 0 && CW % 8 == 0, "warp tile must be a multiple of 8x8");
   static_assert(NS % PF == 0, "prefetch groups must tile a segment");
 };
@@ -299,14 +305,14 @@ struct FragCursor {
 // Forward sweep.  Per interior row j, three segments stream through the same
 // register ring:  seg0 acc += AD_j y_{j-1};  seg1 ser += Tb_{j-1} y_{j-1};
 // seg2 acc += Dinv_j f_g.  (At j = 0, y_{-1} = 0 and seg1 reuses Tb_0.)
-template <int MP, int KT, int WR, int WC>
+template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1>
 __global__ void __launch_bounds__(32 * WR * WC) chain_fwd_kernel(ChainArgs a) {
-  using Cfg = ChainCfg<MP, KT, WR, WC>;
+  using Cfg = ChainCfg<MP, KT, WR, WC, NF_, NY_>;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, LD = Cfg::LD, NT = Cfg::NT, PF = Cfg::PF, GPS = Cfg::GPS;
+  constexpr int NF = Cfg::NF;
   extern __shared__ __align__(16) double sm[];
   double* Ys = sm;
-  double* Fs0 = sm + MP * LD;
-  double* Fs1 = Fs0 + MP * LD;
+  double* Fs = sm + MP * LD;  // ring of NF F tiles
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wr = warp / WC, wc = warp % WC;
@@ -315,7 +321,7 @@ __global__ void __launch_bounds__(32 * WR * WC) chain_fwd_kernel(ChainArgs a) {
   const int64_t c0 = (int64_t)blockIdx.x * KT;
   const int64_t K = a.K;
   const bool vec = (K % 2) == 0;
-  for (int e = tid; e < 3 * MP * LD; e += NT) sm[e] = 0.0;
+  for (int e = tid; e < Cfg::FWD_BUFS * MP * LD; e += NT) sm[e] = 0.0;
   __syncthreads();
 
   const int64_t lo = a.lo[q];
@@ -333,26 +339,35 @@ __global__ void __launch_bounds__(32 * WR * WC) chain_fwd_kernel(ChainArgs a) {
     store_tile(ser, a.base + (int64_t)q * a.base_stride, K, r0, c0 + cw0, MP, g, t, vec);
     return;
   }
-  cp_tile<MP, KT, LD, NT>(Fs0, a.F + (lo + 1) * rowK, K, c0, a.m, vec);
+  // prologue: F rows 0 .. NF-2 in flight (one cp.async group per row, possibly empty)
+#pragma unroll
+  for (int r = 0; r < NF - 1; ++r) {
+    if (r < nint)
+      cp_tile<MP, KT, LD, NT>(Fs + r * MP * LD, a.F + (lo + 1 + r) * rowK, K, c0, a.m, vec);
+    else
+      cp_async_commit();
+  }
 
   FragCursor<MP, PF, GPS, 3> cur;
   cur.seg0 = a.AD + slot0 * blk + r0 * MP;
-  cur.seg1 = a.Tb + slot0 * blk + r0 * MP;  // row j uses Tb_{j-1}: offset below
+  cur.seg1 = a.Tb + slot0 * blk + r0 * MP;  // row j uses Tb_{j-1} (offset below; row 0 reuses Tb_0 x 0)
   cur.seg2 = a.Dinv + slot0 * blk + r0 * MP;
   cur.j = 0; cur.seg = 0; cur.grp = 0; cur.nrows = nint;
-  // Tb_{j-1}: shift seg1 by one block, except row 0 which reuses Tb_0 (times y_{-1} = 0)
   double2 buf[PF][TM];
   group_load<MP, TM, PF>(buf, cur.ptr(), g, t);
-  cp_async_wait_all();
+  cp_async_wait<NF - 2>();
   __syncthreads();
 
   double acc[TM][TN][2];
   zero_acc(acc);
   for (int j = 0; j < nint; ++j) {
     const int64_t gr = lo + 1 + j;
-    const double* Fcur = (j & 1) ? Fs1 : Fs0;
-    double* Fnxt = (j & 1) ? Fs0 : Fs1;
-    if (j + 1 < nint) cp_tile<MP, KT, LD, NT>(Fnxt, a.F + (gr + 1) * rowK, K, c0, a.m, vec);
+    const double* Fcur = Fs + (j % NF) * MP * LD;
+    // refill the slot freed by row j-1 with row j+NF-1
+    if (j + NF - 1 < nint)
+      cp_tile<MP, KT, LD, NT>(Fs + ((j + NF - 1) % NF) * MP * LD, a.F + (gr + NF - 1) * rowK, K, c0, a.m, vec);
+    else
+      cp_async_commit();
 #pragma unroll 1
     for (int seg = 0; seg < 3; ++seg) {
 #pragma unroll 1
@@ -372,22 +387,38 @@ __global__ void __launch_bounds__(32 * WR * WC) chain_fwd_kernel(ChainArgs a) {
     store_smem(acc, Ys, LD, r0, cw0, g, t);
     store_tile(acc, a.X + gr * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
     zero_acc(acc);
-    cp_async_wait_all();
+    cp_async_wait<NF - 2>();  // row j+1's F tile has landed
     __syncthreads();
   }
+  cp_async_wait<0>();
   wgemm<MP, TM, TN, 2>(ser, a.Tb + (slot0 + nint - 1) * blk + r0 * MP, Ys + cw0, LD, g, t);
   store_tile(ser, a.base + (int64_t)q * a.base_stride, K, r0, c0 + cw0, MP, g, t, vec);
 }
 
+// C-layout tile from a shared [MP][LD] tile
+template <int TM, int TN>
+BTD_DEVINL void load_smem(double (&acc)[TM][TN][2], const double* Ys, int ld, int r0, int c0, int g, int t) {
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const double2 v = *reinterpret_cast<const double2*>(&Ys[(r0 + i * 8 + g) * ld + c0 + j * 8 + 2 * t]);
+      acc[i][j][0] = v.x;
+      acc[i][j][1] = v.y;
+    }
+}
+
 // Backward sweep: per row j (descending) two segments through one ring:
 // seg0 acc += G_j x~_q ; seg1 acc += S_j x_{j+1}, with acc initialised to y_j.
-template <int MP, int KT, int WR, int WC>
+template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1>
 __global__ void __launch_bounds__(32 * WR * WC) chain_bwd_kernel(ChainArgs a) {
-  using Cfg = ChainCfg<MP, KT, WR, WC>;
+  using Cfg = ChainCfg<MP, KT, WR, WC, NF_, NY_>;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, LD = Cfg::LD, NT = Cfg::NT, PF = Cfg::PF, GPS = Cfg::GPS;
+  constexpr int NY = Cfg::NY;
   extern __shared__ __align__(16) double sm[];
   double* Xq = sm;
   double* Xn = sm + MP * LD;
+  double* Ysr = sm + 2 * MP * LD;  // ring of NY y tiles (NY > 0)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wr = warp / WC, wc = warp % WC;
@@ -396,7 +427,7 @@ __global__ void __launch_bounds__(32 * WR * WC) chain_bwd_kernel(ChainArgs a) {
   const int64_t c0 = (int64_t)blockIdx.x * KT;
   const int64_t K = a.K;
   const bool vec = (K % 2) == 0;
-  for (int e = tid; e < 2 * MP * LD; e += NT) sm[e] = 0.0;
+  for (int e = tid; e < Cfg::BWD_BUFS * MP * LD; e += NT) sm[e] = 0.0;
   __syncthreads();
 
   const int64_t lo = a.lo[q];
@@ -414,33 +445,48 @@ __global__ void __launch_bounds__(32 * WR * WC) chain_bwd_kernel(ChainArgs a) {
     store_tile(xq, a.X + lo * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
   }
   if (nint <= 0) {
-    cp_async_wait_all();
+    cp_async_wait<0>();
     return;
   }
-  // rows run j = nint-1 .. 0: the stream walks slots downward
+  // rows run j = nint-1 .. 0 (step jj = nint-1-j); y tiles of steps 0..NY-2 in flight
+  if constexpr (NY > 0) {
+#pragma unroll
+    for (int s_ = 0; s_ < NY - 1; ++s_) {
+      if (s_ < nint)
+        cp_tile<MP, KT, LD, NT>(Ysr + s_ * MP * LD, a.X + (lo + nint - s_) * rowK, K, c0, a.m, vec);
+      else
+        cp_async_commit();
+    }
+  }
   FragCursor<MP, PF, GPS, 2> cur;
   cur.seg0 = a.G + (slot0 + nint - 1) * blk + r0 * MP;
   cur.seg1 = a.S + (slot0 + nint - 1) * blk + r0 * MP;
   cur.seg2 = nullptr;
   cur.j = 0; cur.seg = 0; cur.grp = 0; cur.nrows = nint;
   double2 buf[PF][TM];
-  {
-    const double* p0 = cur.ptr();
-    group_load<MP, TM, PF>(buf, p0, g, t);
-  }
+  group_load<MP, TM, PF>(buf, cur.ptr(), g, t);
   double y[TM][TN][2];
-  load_tile(y, a.X + (lo + nint) * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
-  cp_async_wait_all();
+  if constexpr (NY == 0) load_tile(y, a.X + (lo + nint) * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
+  cp_async_wait<(NY > 1 ? NY - 2 : 0)>();
   __syncthreads();
   for (int jj = 0; jj < nint; ++jj) {
     const int j = nint - 1 - jj;
     const int64_t gr = lo + 1 + j;
     double acc[TM][TN][2];
+    if constexpr (NY > 0) {
+      load_smem(acc, Ysr + (jj % NY) * MP * LD, LD, r0, cw0, g, t);
+      if (jj + NY - 1 < nint)
+        cp_tile<MP, KT, LD, NT>(Ysr + ((jj + NY - 1) % NY) * MP * LD, a.X + (gr - (NY - 1)) * rowK, K, c0, a.m,
+                                vec);
+      else
+        cp_async_commit();
+    } else {
 #pragma unroll
-    for (int i = 0; i < TM; ++i)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
-      for (int c = 0; c < TN; ++c) { acc[i][c][0] = y[i][c][0]; acc[i][c][1] = y[i][c][1]; }
-    if (j > 0) load_tile(y, a.X + (gr - 1) * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
+        for (int c = 0; c < TN; ++c) { acc[i][c][0] = y[i][c][0]; acc[i][c][1] = y[i][c][1]; }
+      if (j > 0) load_tile(y, a.X + (gr - 1) * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
+    }
 #pragma unroll 1
     for (int seg = 0; seg < 2; ++seg) {
 #pragma unroll 1
@@ -454,8 +500,10 @@ __global__ void __launch_bounds__(32 * WR * WC) chain_bwd_kernel(ChainArgs a) {
     __syncthreads();
     store_smem(acc, Xn, LD, r0, cw0, g, t);
     store_tile(acc, a.X + gr * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
+    if constexpr (NY > 1) cp_async_wait<NY - 2>();
     __syncthreads();
   }
+  cp_async_wait<0>();
 }
 
 }  // namespace btd

@@ -37,6 +37,8 @@ BTD_DEVINL void cp_async8(void* smem_dst, const void* gmem_src) {
 }
 BTD_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 BTD_DEVINL void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+template <int N>
+BTD_DEVINL void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // 16B read-only streaming load of a factor fragment (L2-resident factors,
 // re-read by the CTAs that share a range; keep them out of L1).

@@ -1,0 +1,11 @@
+#!/bin/bash
+run() {
+  python bench.py --steps 5 --warmup 2 --no-e2e --no-cpu "$@" 2>/dev/null | python -c "
+import json,sys
+d=json.loads(sys.stdin.read()); c=d['config']
+print(c['workload'], 'P=%d split=%d'%(c['ranks'],c['split']), 'RHS/s=%.0f'%d['value'], 'ms=%.2f'%d['ms_per_step'], 'fwd=%.2f tree=%.2f bwd=%.2f'%(d['phases_ms']['forward'],d['phases_ms']['interface_tree'],d['phases_ms']['backward']), 'solve_frac=%.3f'%d['solve_roofline']['frac'], 'res=%.1e'%(d['rel_residual'] or -1))"
+}
+python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+for c in c1 c2 c4 c0; do echo -n "v0 "; run --config $c; done
+echo -n "v1 "; BTD_CHAIN_VARIANT=1 run --config c1
+echo -n "v1 "; BTD_CHAIN_VARIANT=1 run --config c2
