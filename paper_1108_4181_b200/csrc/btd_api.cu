@@ -214,11 +214,26 @@ Term term(Opnd A, Opnd B, int64_t k, double alpha = 1.0, const int64_t* k_arr = 
   return t;
 }
 
+// Segmented split-K maps for one batched GEMM (built at plan time).
+struct SplitK {
+  int ntotal = 0;
+  int64_t kchunk = 0;
+  const int32_t *sb = nullptr, *sk = nullptr, *zoff = nullptr, *zcnt = nullptr;
+  double* partial = nullptr;
+};
+
 void launch_gemm(int64_t rows, int64_t cols, int nbatch, Opnd C, Opnd Cin, double beta,
-                 std::initializer_list<Term> terms, cudaStream_t st) {
+                 std::initializer_list<Term> terms, cudaStream_t st, const SplitK* sp = nullptr) {
   if (nbatch <= 0 || rows <= 0 || cols <= 0) return;
   GemmDesc d;
   memset(&d, 0, sizeof d);
+  if (sp && sp->ntotal > 0) {
+    d.split_b = sp->sb;
+    d.split_k = sp->sk;
+    d.kchunk = sp->kchunk;
+    d.partial = sp->partial;
+    d.nsplit_total = sp->ntotal;
+  }
   d.rows = rows;
   d.cols = cols;
   d.nbatch = nbatch;
@@ -227,15 +242,56 @@ void launch_gemm(int64_t rows, int64_t cols, int nbatch, Opnd C, Opnd Cin, doubl
   d.beta = beta;
   d.nterms = 0;
   for (const Term& t : terms) d.t[d.nterms++] = t;
-  const int gz = std::min(nbatch, 65535);
-  if (rows <= 32 || cols <= 32) {
-    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32), gz);
-    gemm_batched_kernel<32, 32><<<grid, 128, 0, st>>>(d);
-  } else {
+  const int gz = std::min(d.split_b ? d.nsplit_total : nbatch, 65535);
+  static int legacy = -1;
+  if (legacy < 0) {
+    const char* e = getenv("BTD_GEMM_LEGACY");
+    legacy = e ? atoi(e) : 0;
+  }
+  if (legacy && !d.split_b) {
+    if (rows <= 32 || cols <= 32) {
+      dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32), gz);
+      gemm_batched_kernel<32, 32><<<grid, 128, 0, st>>>(d);
+    } else {
+      dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64), gz);
+      gemm_batched_kernel<64, 64><<<grid, 128, 0, st>>>(d);
+    }
+    CK_LAUNCH();
+    return;
+  }
+  auto tiles = [&](int64_t bm, int64_t bn) { return ((rows + bm - 1) / bm) * ((cols + bn - 1) / bn) * gz; };
+  if (rows >= 128 && cols >= 64 && tiles(128, 64) >= 148) {
+    using C_ = PipeCfg<128, 64, 4, 2, 3>;
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(gemm_pipe_kernel<128, 64, 4, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)C_::SMEM));
+      attr = true;
+    }
+    dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 127) / 128), gz);
+    gemm_pipe_kernel<128, 64, 4, 2, 3><<<grid, C_::NT, C_::SMEM, st>>>(d);
+  } else if (rows > 32 && cols > 32) {
+    using C_ = PipeCfg<64, 64, 2, 2, 4>;
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(gemm_pipe_kernel<64, 64, 2, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)C_::SMEM));
+      attr = true;
+    }
     dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64), gz);
-    gemm_batched_kernel<64, 64><<<grid, 128, 0, st>>>(d);
+    gemm_pipe_kernel<64, 64, 2, 2, 4><<<grid, C_::NT, C_::SMEM, st>>>(d);
+  } else {
+    using C_ = PipeCfg<32, 32, 2, 2, 3>;
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32), gz);
+    gemm_pipe_kernel<32, 32, 2, 2, 3><<<grid, C_::NT, C_::SMEM, st>>>(d);
   }
   CK_LAUNCH();
+  if (d.split_b) {
+    const int64_t per = rows * cols;
+    dim3 grid((unsigned)std::min<int64_t>((per + 255) / 256, 64), (unsigned)std::min(nbatch, 65535));
+    splitk_reduce_kernel<<<grid, 256, 0, st>>>(sp->partial, sp->zoff, sp->zcnt, C, Cin, beta, rows, cols, nbatch);
+    CK_LAUNCH();
+  }
 }
 
 struct Node {
@@ -294,11 +350,16 @@ struct btd_plan {
   // nodes this rank needs (its own interfaces + dependency closure), z batch over them
   int nz = 0;
   const int64_t *z_id = nullptr, *z_roff = nullptr, *z_rld = nullptr, *z_nlo = nullptr;
+  SplitK z_split;
+  std::vector<int64_t> z_k;  // reduction length per z entry (host)
   struct Level {
     int count = 0;
     const int64_t *c_idx = nullptr, *z_idx = nullptr, *e_idx = nullptr, *xl_idx = nullptr,
                   *h_idx = nullptr, *xh_idx = nullptr;
+    SplitK split;
   };
+  int64_t partial_elems_per_k = 0;  // split-K scratch: doubles per unit K
+  DevBuf partial;
   std::vector<Level> levels;
   // interface-RHS carry (local ranges whose last interior row exists)
   int ncarry = 0;
@@ -783,6 +844,50 @@ void build_local(btd_plan& pl, const double* diag, const double* lower, const do
   CK(cudaStreamSynchronize(st));
 }
 
+// Choose k-chunks so a tree launch fills >= 2 waves; record (entry, chunk) maps.
+SplitK make_split(btd_plan& pl, const std::vector<int64_t>& kper, int64_t tiles_per_entry, int64_t& maxz) {
+  SplitK sp;
+  const int64_t want = 2 * 148;
+  int64_t base = 0, kmax = 0;
+  for (int64_t k : kper) { base += tiles_per_entry; kmax = std::max(kmax, k); }
+  if (kper.empty() || base >= want * 2) return sp;
+  // chunk: the largest multiple of 16 that still yields >= want CTAs in total (and >= 64 long)
+  int64_t chunk = std::max<int64_t>(64, (kmax + 15) / 16 * 16);
+  auto total = [&](int64_t ch) {
+    int64_t t = 0;
+    for (int64_t k : kper) t += (k + ch - 1) / ch;
+    return t;
+  };
+  while (chunk > 64 && total(chunk) * tiles_per_entry < want) chunk = std::max<int64_t>(64, (chunk / 2 + 15) / 16 * 16);
+  const int64_t nt = total(chunk);
+  if (nt <= (int64_t)kper.size()) return sp;  // no entry split: plain launch
+  std::vector<int32_t> sb, sk, zoff, zcnt;
+  for (size_t b = 0; b < kper.size(); ++b) {
+    const int64_t n = std::max<int64_t>(1, (kper[b] + chunk - 1) / chunk);
+    zoff.push_back((int32_t)sb.size());
+    zcnt.push_back((int32_t)n);
+    for (int64_t c = 0; c < n; ++c) { sb.push_back((int32_t)b); sk.push_back((int32_t)c); }
+  }
+  sp.ntotal = (int)sb.size();
+  sp.kchunk = chunk;
+  sp.sb = pl.upload(sb); sp.sk = pl.upload(sk); sp.zoff = pl.upload(zoff); sp.zcnt = pl.upload(zcnt);
+  maxz = std::max<int64_t>(maxz, sp.ntotal);
+  return sp;
+}
+
+void build_splits(btd_plan& pl) {
+  const int64_t mp = pl.mp;
+  // tiles per entry for an (mp x K) output; K unknown at plan time: assume one column tile per 64
+  const int64_t tiles = std::max<int64_t>(1, (mp + 63) / 64);
+  int64_t maxz = 0;
+  pl.z_split = make_split(pl, pl.z_k, tiles, maxz);
+  for (auto& L_ : pl.levels) {
+    std::vector<int64_t> kk(L_.count, mp);
+    L_.split = make_split(pl, kk, tiles, maxz);
+  }
+  pl.partial_elems_per_k = maxz * mp;
+}
+
 // ---------------------------------------------------------------- plan build, global part
 // contrib_all: [nr][4][mp][mp] device, identical on every rank.
 void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int64_t* err_row) {
@@ -996,6 +1101,9 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
       L_.c_idx = pl.upload(c); L_.z_idx = pl.upload(z); L_.e_idx = pl.upload(e);
       L_.xl_idx = pl.upload(xl); L_.h_idx = pl.upload(h); L_.xh_idx = pl.upload(xh);
     }
+    // split-K plans: enough CTAs (>= 2 waves) for the series sums and the level corrections
+    pl.z_k = zrl;
+    build_splits(pl);
   }
   CK(cudaStreamSynchronize(st));
   pl.factor_bytes += (int64_t)(rtot + 2 * nn * blk) * sizeof(double);
@@ -1011,6 +1119,11 @@ void ensure_scratch(btd_plan& pl, int64_t K) {
   pl.xt.alloc((size_t)(pl.nr + 1) * mpK * sizeof(double));
   CK(cudaMemset(pl.xt.p, 0, (size_t)(pl.nr + 1) * mpK * sizeof(double)));
   CK(cudaMemset(pl.ft.p, 0, (size_t)pl.nr * mpK * sizeof(double)));
+  if (pl.partial_elems_per_k) {
+    pl.partial.alloc((size_t)pl.partial_elems_per_k * K * sizeof(double));
+    pl.z_split.partial = pl.partial.d();
+    for (auto& L_ : pl.levels) L_.split.partial = pl.partial.d();
+  }
   pl.scratch_k = K;
 }
 
@@ -1071,12 +1184,13 @@ void solve_tree(btd_plan& pl, int64_t K, cudaStream_t st) {
   double* xt = pl.xt.d();
   double* z = pl.zbuf.d();
   launch_gemm(mp, K, pl.nz, mk(z, pl.z_id, 0, mpK, K), none(), 0.0,
-              {term(mk(pl.Rrows.d(), pl.z_roff, 0, 1, 0, pl.z_rld), mk(ft, pl.z_nlo, 0, mpK, K), 0, 1.0, pl.z_rld)}, st);
+              {term(mk(pl.Rrows.d(), pl.z_roff, 0, 1, 0, pl.z_rld), mk(ft, pl.z_nlo, 0, mpK, K), 0, 1.0, pl.z_rld)}, st,
+              &pl.z_split);
   for (const auto& lev : pl.levels)
     launch_gemm(mp, K, lev.count, mk(xt, lev.c_idx, 0, mpK, K), mk(z, lev.z_idx, 0, mpK, K), 1.0,
                 {term(mk(pl.EH.d(), lev.e_idx, 0, blk, mp), mk(xt, lev.xl_idx, 0, mpK, K), mp),
                  term(mk(pl.EH.d(), lev.h_idx, 0, blk, mp), mk(xt, lev.xh_idx, 0, mpK, K), mp)},
-                st);
+                st, &lev.split);
 }
 
 // Backward sweeps of the owned ranges (x~ known), x[lo_q] = x~_q.

@@ -39,6 +39,13 @@ struct Term {
 struct GemmDesc {
   int64_t rows, cols;
   int nbatch;
+  // segmented split-K: grid.z enumerates (entry, k-chunk) pairs; partial sums go to
+  // partial + z*rows*cols and a fixed-order reduction finishes C (deterministic)
+  const int32_t* split_b;
+  const int32_t* split_k;
+  int64_t kchunk;
+  double* partial;
+  int nsplit_total;
   Opnd C;
   Opnd Cin;               // Cin.base == nullptr -> no addend
   double beta;
@@ -162,6 +169,179 @@ __global__ void __launch_bounds__(128) gemm_batched_kernel(GemmDesc d) {
             C[r * ldc + c] = val;
           }
         }
+  }
+}
+
+// cp.async with zero fill: copies `src_bytes` (0..size) and zero-fills the rest
+BTD_DEVINL void cp_async16_z(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes));
+}
+BTD_DEVINL void cp_async8_z(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes));
+}
+
+// Pipelined variant: STAGES-deep cp.async ring of (A: BM x 16, B: 16 x BN) slabs,
+// warps WGM x WGN with 32x32 (or 16x16) warp tiles, DMMA m8n8k4.
+template <int BM, int BN, int WGM, int WGN, int STAGES>
+struct PipeCfg {
+  static constexpr int NT = 32 * WGM * WGN;
+  static constexpr int BK = 16;
+  static constexpr int LDA = 24;       // A row pitch (doubles): 12 double2 == 4 (mod 8)
+  static constexpr int LDB = BN + 2;   // B row pitch: == 2 (mod 16)
+  static constexpr int WTM = BM / WGM, WTN = BN / WGN;
+  static constexpr int TM = WTM / 8, TN = WTN / 8;
+  static constexpr int A_ELEMS = BM * LDA, B_ELEMS = BK * LDB;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE * sizeof(double);
+};
+
+template <int BM, int BN, int WGM, int WGN, int STAGES>
+__global__ void __launch_bounds__(32 * WGM * WGN) gemm_pipe_kernel(GemmDesc d) {
+  using C_ = PipeCfg<BM, BN, WGM, WGN, STAGES>;
+  constexpr int NT = C_::NT, BK = C_::BK, LDA = C_::LDA, LDB = C_::LDB, TM = C_::TM, TN = C_::TN;
+  extern __shared__ __align__(16) double smp[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp / WGN, wn = warp % WGN;
+  const int64_t row0 = (int64_t)blockIdx.y * BM, col0 = (int64_t)blockIdx.x * BN;
+
+  const int nz = d.split_b ? d.nsplit_total : d.nbatch;
+  for (int zz = blockIdx.z; zz < nz; zz += gridDim.z) {
+    const int b = d.split_b ? d.split_b[zz] : zz;
+    double acc[TM][TN][2];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int ti = 0; ti < d.nterms; ++ti) {
+      const Term& tm_ = d.t[ti];
+      const double* A = opnd_ptr(tm_.A, b);
+      const double* B = opnd_ptr(tm_.B, b);
+      const int64_t lda = opnd_ld(tm_.A, b), ldb = opnd_ld(tm_.B, b);
+      int64_t K = tm_.k_arr ? tm_.k_arr[b] : tm_.k;
+      const double alpha = tm_.alpha;
+      if (d.split_b) {  // this CTA's k-chunk: shift the operands, clip K
+        const int64_t k0 = (int64_t)d.split_k[zz] * d.kchunk;
+        A += k0;
+        B += k0 * ldb;
+        K = K - k0 < d.kchunk ? K - k0 : d.kchunk;
+      }
+      if (K <= 0) continue;
+      const bool va = ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+      const bool vb = ((ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
+      const int nk = (int)((K + BK - 1) / BK);
+      auto load = [&](int kt, int slot) {
+        double* As = smp + slot * C_::STAGE;
+        double* Bs = As + C_::A_ELEMS;
+        const int64_t k0 = (int64_t)kt * BK;
+        // A: BM rows x 16 k  (8 chunks of 2 doubles per row)
+        for (int e = tid; e < BM * 8; e += NT) {
+          const int r = e >> 3, ch = (e & 7) * 2;
+          const int64_t gr = row0 + r, gk = k0 + ch;
+          double* dst = As + r * LDA + ch;
+          const int64_t rem = (gr < d.rows) ? K - gk : 0;
+          const double* src = (rem > 0) ? A + gr * lda + gk : A;
+          if (va) {
+            cp_async16_z(dst, src, rem >= 2 ? 16 : (rem == 1 ? 8 : 0));
+          } else {
+            cp_async8_z(dst, src, rem >= 1 ? 8 : 0);
+            cp_async8_z(dst + 1, rem >= 2 ? src + 1 : src, rem >= 2 ? 8 : 0);
+          }
+        }
+        // B: 16 k x BN cols
+        for (int e = tid; e < BK * (BN / 2); e += NT) {
+          const int kk = e / (BN / 2), ch = (e % (BN / 2)) * 2;
+          const int64_t gk = k0 + kk, gc = col0 + ch;
+          double* dst = Bs + kk * LDB + ch;
+          const int64_t rem = (gk < K) ? d.cols - gc : 0;
+          const double* src = (rem > 0) ? B + gk * ldb + gc : B;
+          if (vb) {
+            cp_async16_z(dst, src, rem >= 2 ? 16 : (rem == 1 ? 8 : 0));
+          } else {
+            cp_async8_z(dst, src, rem >= 1 ? 8 : 0);
+            cp_async8_z(dst + 1, rem >= 2 ? src + 1 : src, rem >= 2 ? 8 : 0);
+          }
+        }
+      };
+#pragma unroll
+      for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < nk) load(s, s);
+        cp_async_commit();
+      }
+      for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        if (kt + STAGES - 1 < nk) load(kt + STAGES - 1, (kt + STAGES - 1) % STAGES);
+        cp_async_commit();
+        const double* As = smp + (kt % STAGES) * C_::STAGE;
+        const double* Bs = As + C_::A_ELEMS;
+#pragma unroll
+        for (int s = 0; s < BK / 8; ++s) {
+          double2 a[TM];
+          double b0[TN], b1[TN];
+#pragma unroll
+          for (int i = 0; i < TM; ++i) {
+            a[i] = *reinterpret_cast<const double2*>(&As[(wm * C_::WTM + i * 8 + g) * LDA + 8 * s + 2 * t]);
+            if (alpha != 1.0) { a[i].x *= alpha; a[i].y *= alpha; }
+          }
+#pragma unroll
+          for (int j = 0; j < TN; ++j) {
+            b0[j] = Bs[(8 * s + 2 * t) * LDB + wn * C_::WTN + j * 8 + g];
+            b1[j] = Bs[(8 * s + 2 * t + 1) * LDB + wn * C_::WTN + j * 8 + g];
+          }
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b0[j]);
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b1[j]);
+        }
+      }
+      cp_async_wait<0>();
+      __syncthreads();
+    }
+    double* C = d.split_b ? d.partial + (int64_t)zz * d.rows * d.cols : const_cast<double*>(opnd_ptr(d.C, b));
+    const int64_t ldc = d.split_b ? d.cols : opnd_ld(d.C, b);
+    const double* Ci = (!d.split_b && d.Cin.base) ? opnd_ptr(d.Cin, b) : nullptr;
+    const int64_t ldci = Ci ? opnd_ld(d.Cin, b) : 0;
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int64_t r = row0 + wm * C_::WTM + i * 8 + g;
+          const int64_t c = col0 + wn * C_::WTN + j * 8 + 2 * t + v;
+          if (r < d.rows && c < d.cols) {
+            double val = acc[i][j][v];
+            if (Ci) val += d.beta * Ci[r * ldci + c];
+            C[r * ldc + c] = val;
+          }
+        }
+  }
+}
+
+// C_b = beta * Cin_b + sum_{z in [zoff_b, zoff_b + nz_b)} partial_z   (fixed order)
+__global__ void splitk_reduce_kernel(const double* partial, const int32_t* zoff, const int32_t* zcnt, Opnd C, Opnd Cin,
+                                     double beta, int64_t rows, int64_t cols, int nbatch) {
+  const int64_t per = rows * cols;
+  for (int b = blockIdx.y; b < nbatch; b += gridDim.y) {
+    double* Cb = const_cast<double*>(opnd_ptr(C, b));
+    const int64_t ldc = opnd_ld(C, b);
+    const double* Ci = Cin.base ? opnd_ptr(Cin, b) : nullptr;
+    const int64_t ldci = Ci ? opnd_ld(Cin, b) : 0;
+    const double* P = partial + (int64_t)zoff[b] * per;
+    const int n = zcnt[b];
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per; e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t r = e / cols, c = e % cols;
+      double v = 0.0;
+      for (int z = 0; z < n; ++z) v += P[(int64_t)z * per + e];
+      if (Ci) v += beta * Ci[r * ldci + c];
+      Cb[r * ldc + c] = v;
+    }
   }
 }
 
