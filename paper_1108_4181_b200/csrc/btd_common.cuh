@@ -40,6 +40,14 @@ BTD_DEVINL void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::
 template <int N>
 BTD_DEVINL void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+BTD_DEVINL void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); }
+
+// L2 prefetch of `bytes` contiguous bytes by the lanes of one warp (128 B lines)
+BTD_DEVINL void warp_prefetch_l2(const void* p, int64_t bytes, int lane) {
+  const char* c = static_cast<const char*>(p);
+  for (int64_t o = (int64_t)lane * 128; o < bytes; o += 32 * 128) prefetch_l2(c + o);
+}
+
 // 16B read-only streaming load of a factor fragment (L2-resident factors,
 // re-read by the CTAs that share a range; keep them out of L1).
 BTD_DEVINL double2 ldg_cg2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
