@@ -548,10 +548,46 @@ void launch_chain_t(const ChainArgs& a, bool fwd, cudaStream_t st) {
   CK_LAUNCH();
 }
 
+template <int MP, int NW, int NSTG>
+void launch_stream_t(const ChainArgs& a, bool fwd, cudaStream_t st) {
+  using C = StreamCfg<MP, NW, NSTG>;
+  const size_t smem = fwd ? C::FWD_SMEM : C::BWD_SMEM;
+  dim3 grid((unsigned)((a.K + C::KC - 1) / C::KC), (unsigned)a.nr);
+  if (fwd) {
+    CK(cudaFuncSetAttribute(stream_fwd_kernel<MP, NW, NSTG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    stream_fwd_kernel<MP, NW, NSTG><<<grid, C::NT, smem, st>>>(a);
+  } else {
+    CK(cudaFuncSetAttribute(stream_bwd_kernel<MP, NW, NSTG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    stream_bwd_kernel<MP, NW, NSTG><<<grid, C::NT, smem, st>>>(a);
+  }
+  CK_LAUNCH();
+}
+
+// Streamed (TMA bulk-copy) sweeps for MP <= 32: needs 16-byte aligned rows (even K).
+bool launch_stream(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char* e = getenv("BTD_STREAM");
+    enabled = e ? atoi(e) : 1;
+  }
+  if (!enabled || mp > 32 || (a.K & 1) || (reinterpret_cast<uintptr_t>(a.F) & 15) ||
+      (reinterpret_cast<uintptr_t>(a.X) & 15))
+    return false;
+  const bool wide = a.K > 32;
+  switch (mp) {
+    case 8: wide ? launch_stream_t<8, 4, 3>(a, fwd, st) : launch_stream_t<8, 2, 3>(a, fwd, st); break;
+    case 16: wide ? launch_stream_t<16, 4, 3>(a, fwd, st) : launch_stream_t<16, 2, 3>(a, fwd, st); break;
+    case 32: wide ? launch_stream_t<32, 4, 2>(a, fwd, st) : launch_stream_t<32, 2, 2>(a, fwd, st); break;
+    default: return false;
+  }
+  return true;
+}
+
 // Chain-kernel configuration per padded block order (MP, KT, warp rows x warp cols).
 // BTD_CHAIN_VARIANT selects alternatives for tuning experiments.
 void launch_chain(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
   if (a.nr <= 0) return;
+  if (launch_stream(mp, a, fwd, st)) return;
   static int variant = -1;
   if (variant < 0) {
     const char* e = getenv("BTD_CHAIN_VARIANT");

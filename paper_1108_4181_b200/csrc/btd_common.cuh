@@ -51,3 +51,28 @@ BTD_DEVINL void warp_prefetch_l2(const void* p, int64_t bytes, int lane) {
 // 16B read-only streaming load of a factor fragment (L2-resident factors,
 // re-read by the CTAs that share a range; keep them out of L1).
 BTD_DEVINL double2 ldg_cg2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
+
+// ---- mbarrier + bulk async copy (TMA engine, 1-D) ------------------------------
+BTD_DEVINL void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+BTD_DEVINL void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+BTD_DEVINL void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::); }
+BTD_DEVINL void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes));
+}
+BTD_DEVINL void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+// global -> shared bulk copy, completion counted on `bar` (bytes % 16 == 0, 16B-aligned)
+BTD_DEVINL void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
