@@ -380,6 +380,18 @@ struct btd_plan {
   std::mutex mu;
   cudaStream_t last_stream = nullptr;
   int64_t factor_bytes = 0;
+  // CUDA graphs of repeated solves: key (F, X, K) -> instantiated graph on the plan's stream
+  struct GraphEntry {
+    const double* F;
+    double* X;
+    int64_t K;
+    int calls;
+    cudaGraphExec_t exec;
+    int64_t nkern;
+  };
+  std::vector<GraphEntry> graphs;
+  cudaStream_t own = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   // cuSOLVER for block orders above 256 (preprocessing only)
   cusolverDnHandle_t solver = nullptr;
   DevBuf sv_work, sv_ipiv, sv_info, sv_lu;
@@ -416,6 +428,11 @@ struct btd_plan {
     for (auto e : ev_pending) cudaEventDestroy(e);
     for (auto e : ev_free) cudaEventDestroy(e);
     if (solver) cusolverDnDestroy(solver);
+    for (auto& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (own) cudaStreamDestroy(own);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
   }
   template <class T>
   const T* upload(const std::vector<T>& v) {
@@ -1149,6 +1166,9 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
 // ---------------------------------------------------------------- solve
 void ensure_scratch(btd_plan& pl, int64_t K) {
   if (pl.scratch_k == K) return;
+  for (auto& g : pl.graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  pl.graphs.clear();  // captured graphs point at the old scratch
   const int64_t mpK = pl.mp * K;
   pl.ft.alloc((size_t)pl.nr * mpK * sizeof(double));
   pl.zbuf.alloc((size_t)pl.nodes.size() * mpK * sizeof(double));
@@ -1268,6 +1288,63 @@ void solve_device(btd_plan& pl, const double* F, double* X, int64_t K, cudaStrea
   pl.ev_mark(st);
   solve_backward(pl, F, X, K, st);
   pl.ev_mark(st);
+}
+
+// Repeated (F, X, K) solves replay a CUDA graph of the whole launch sequence
+// (captured on the plan's own stream at the second call, after the first call
+// has set kernel attributes and scratch); the caller's stream is joined with events.
+void solve_graphed(btd_plan& pl, const double* F, double* X, int64_t K, cudaStream_t st) {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char* e = getenv("BTD_GRAPHS");
+    enabled = e ? atoi(e) : 1;
+  }
+  if (!enabled || pl.profiling) {
+    solve_device(pl, F, X, K, st);
+    return;
+  }
+  btd_plan::GraphEntry* ge = nullptr;
+  for (auto& g : pl.graphs)
+    if (g.F == F && g.X == X && g.K == K) ge = &g;
+  if (!ge) {
+    if (pl.graphs.size() >= 8) {  // bounded cache
+      if (pl.graphs.front().exec) cudaGraphExecDestroy(pl.graphs.front().exec);
+      pl.graphs.erase(pl.graphs.begin());
+    }
+    pl.graphs.push_back({F, X, K, 0, nullptr, 0});
+    ge = &pl.graphs.back();
+  }
+  if (++ge->calls < 2) {
+    solve_device(pl, F, X, K, st);
+    return;
+  }
+  if (!pl.own) {
+    CK(cudaStreamCreateWithFlags(&pl.own, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&pl.ev_in, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&pl.ev_out, cudaEventDisableTiming));
+  }
+  if (!ge->exec) {
+    cudaGraph_t graph;
+    const int64_t l0 = g_launches.load();
+    CK(cudaStreamBeginCapture(pl.own, cudaStreamCaptureModeThreadLocal));
+    try {
+      solve_device(pl, F, X, K, pl.own);
+    } catch (...) {
+      cudaStreamEndCapture(pl.own, &graph);
+      throw;
+    }
+    CK(cudaStreamEndCapture(pl.own, &graph));
+    ge->nkern = g_launches.load() - l0;
+    g_launches.fetch_sub(ge->nkern);  // counted when the graph runs, not when captured
+    CK(cudaGraphInstantiate(&ge->exec, graph, 0));
+    CK(cudaGraphDestroy(graph));
+  }
+  CK(cudaEventRecord(pl.ev_in, st));
+  CK(cudaStreamWaitEvent(pl.own, pl.ev_in, 0));
+  CK(cudaGraphLaunch(ge->exec, pl.own));
+  g_launches.fetch_add(ge->nkern);
+  CK(cudaEventRecord(pl.ev_out, pl.own));
+  CK(cudaStreamWaitEvent(st, pl.ev_out, 0));
 }
 
 // Sharded phase A: local sweeps, then this rank's (base, carry) pairs into exch [nrl][2][mp][K].
@@ -1426,7 +1503,7 @@ int btd_plan_solve(btd_plan* pl, const double* f, double* x, int64_t k, void* st
   if (pl->world != 1) { g_err = "sharded plan: use btd_shard_solve_a/b"; return BTD_ERR_INVALID_ARG; }
   return guarded(pl, stream, [&](cudaStream_t st) {
     ensure_scratch(*pl, k);
-    solve_device(*pl, f, x, k, st);
+    solve_graphed(*pl, f, x, k, st);
   });
 }
 
@@ -1437,12 +1514,15 @@ int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int6
   return guarded(pl, stream, [&](cudaStream_t st) {
     const size_t bytes = (size_t)pl->n * pl->m * k * sizeof(double);
     if (pl->hostio_k != k) {
+      for (auto& g : pl->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+      pl->graphs.clear();
       pl->hostio.alloc(bytes);
       pl->hostio_k = k;
     }
     ensure_scratch(*pl, k);
     CK(cudaMemcpyAsync(pl->hostio.p, f_host, bytes, cudaMemcpyHostToDevice, st));
-    solve_device(*pl, pl->hostio.d(), pl->hostio.d(), k, st);
+    solve_graphed(*pl, pl->hostio.d(), pl->hostio.d(), k, st);
     CK(cudaMemcpyAsync(x_host, pl->hostio.p, bytes, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   });

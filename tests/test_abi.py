@@ -58,3 +58,10 @@ def test_status_codes_map_to_reference_errors():
         _native.check(3)
     with pytest.raises(errors.DeviceError):
         _native.check(4)
+
+
+def test_sass_has_tma_bulk_copies_and_mbarriers():
+    build.build()
+    out = subprocess.run(["cuobjdump", "-sass", _native.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UBLKCP" in out, "TMA bulk-copy path missing from SASS"
+    assert "SYNCS" in out, "mbarrier path missing from SASS"
