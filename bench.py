@@ -51,8 +51,9 @@ BENCH_CFG = {
     "c1": dict(subdomains_per_gpu=lambda w: 18, ranges_per_gpu=18),
     "c2": dict(subdomains_per_gpu=lambda w: 9, ranges_per_gpu=9),
     # c3: the explicit interface Schur complement S (N=63, M=2048) of the 64-subdomain
-    # Helmholtz DD; P = 8 ranges of 8 interface rows (a multiple of 1/2/4/8 GPUs)
-    "c3": dict(subdomains_per_gpu=lambda w: 8 // w, ranges_per_gpu=8),
+    # Helmholtz DD; P = 9 ranges of 7 interface rows on one GPU (288 GEMM tiles fill the
+    # 296 CTA slots), P = 8 (a multiple of 2/4/8) when sharded
+    "c3": dict(subdomains_per_gpu=lambda w: 9 if w == 1 else 8 // w, ranges_per_gpu=8),
     "c4": dict(subdomains_per_gpu=lambda w: 8 * w, ranges_per_gpu=592),
 }
 

@@ -85,20 +85,28 @@ int btd_plan_solve_host(btd_plan* plan, const double* f_host, double* x_host, in
                         void* stream);
 
 int btd_plan_destroy(btd_plan* plan);
+int btd_plan_query(const btd_plan* plan, btd_plan_info* info);
 
 /* ---- row-sharded (multi-GPU) plans and solves --------------------------
  * The ranges (ranks*split of them, a multiple of `world`) are split
  * contiguously over `world` processes, one GPU each; rank r owns ranges
  * [r*P/world, (r+1)*P/world) and their block rows.  The reference's
- * distributed solve (harness.py:147-216: local sweep, allgather of the
- * (base, carry) interface pairs, reduced solve, local recovery) maps to:
+ * distributed solve (harness.py:147-216: local sweep, exchange of the
+ * interface pairs, reduced solve, local recovery) maps to:
  *   plan:  btd_plan_create_shard (local factors + this shard's four
  *          reduced-system contributions per range) -> caller all-gathers the
- *          contributions (btd_shard_contrib) over NCCL -> btd_shard_finish
- *          (reduced system + partition tree, identical on every rank);
- *   solve: btd_shard_solve_a (local sweeps; writes this shard's (base, carry)
- *          pairs, btd_shard_exchange_size doubles) -> caller all-gathers them
- *          -> btd_shard_solve_b (interface RHS, tree, local recovery).
+ *          contributions (btd_shard_contrib) -> btd_shard_finish (reduced
+ *          system + partition tree, identical on every rank);
+ *   solve: btd_shard_solve_a (local sweeps; emits the carry of its last range,
+ *          n_carry doubles) -> caller all-gathers the carries ->
+ *          btd_shard_solve_b (interface RHS of its ranges; partial series sums
+ *          R_node f~ over its own ranges for the tree nodes whose segment
+ *          crosses a rank boundary, n_partial doubles) -> caller all-gathers
+ *          the partials -> btd_shard_solve_c (sums them in rank order, tree
+ *          levels for the nodes it needs, local recovery).
+ *   This is the paper's "sum of a series over distributed data": per solve a
+ *   rank exchanges M*K + (#crossing nodes)*M*K doubles, not the reference
+ *   harness's all-gather of every range's pair.
  * f_local / x_local hold the shard's rows [row_lo, row_hi) (btd_plan_query).
  * err_info[0] = SingularPivot row, err_info[1] = failing global range. */
 int btd_plan_create_shard(const double* diag, const double* lower, const double* upper,
@@ -109,12 +117,13 @@ int btd_plan_create_shard(const double* diag, const double* lower, const double*
  * buffer dst (dst == NULL: only report *nelems) */
 int btd_shard_contrib(btd_plan* plan, double* dst, int64_t* nelems, void* stream);
 int btd_shard_finish(btd_plan* plan, const double* contrib_all, void* stream, int64_t* err_row);
-int btd_shard_exchange_size(const btd_plan* plan, int64_t k, int64_t* nelems_local);
+int btd_shard_exchange_size(const btd_plan* plan, int64_t k, int64_t* n_carry, int64_t* n_partial);
 int btd_shard_solve_a(btd_plan* plan, const double* f_local, double* x_local, int64_t k,
-                      double* exch_local, void* stream);
-int btd_shard_solve_b(btd_plan* plan, const double* exch_all, const double* f_local,
+                      double* carry_out, void* stream);
+int btd_shard_solve_b(btd_plan* plan, const double* carry_all, double* partial_out, int64_t k,
+                      void* stream);
+int btd_shard_solve_c(btd_plan* plan, const double* partial_all, const double* f_local,
                       double* x_local, int64_t k, void* stream);
-int btd_plan_query(const btd_plan* plan, btd_plan_info* info);
 
 /* Per-phase device timing of solves (CUDA events recorded on the solve
  * stream between the forward sweep, the interface/tree phase and the backward

@@ -35,6 +35,7 @@ EXPORTS = (
     "btd_shard_exchange_size",
     "btd_shard_solve_a",
     "btd_shard_solve_b",
+    "btd_shard_solve_c",
     "btd_plan_set_profiling",
     "btd_plan_phase_times",
     "btd_launch_count",
@@ -86,12 +87,14 @@ def load():
     lib.btd_shard_contrib.restype = i32
     lib.btd_shard_finish.argtypes = [vp, dp, vp, ctypes.POINTER(i64)]
     lib.btd_shard_finish.restype = i32
-    lib.btd_shard_exchange_size.argtypes = [vp, i64, ctypes.POINTER(i64)]
+    lib.btd_shard_exchange_size.argtypes = [vp, i64, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.btd_shard_exchange_size.restype = i32
     lib.btd_shard_solve_a.argtypes = [vp, dp, dp, i64, dp, vp]
     lib.btd_shard_solve_a.restype = i32
-    lib.btd_shard_solve_b.argtypes = [vp, dp, dp, dp, i64, vp]
+    lib.btd_shard_solve_b.argtypes = [vp, dp, dp, i64, vp]
     lib.btd_shard_solve_b.restype = i32
+    lib.btd_shard_solve_c.argtypes = [vp, dp, dp, dp, i64, vp]
+    lib.btd_shard_solve_c.restype = i32
     lib.btd_plan_set_profiling.argtypes = [vp, i32]
     lib.btd_plan_set_profiling.restype = i32
     lib.btd_plan_phase_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64), i32]

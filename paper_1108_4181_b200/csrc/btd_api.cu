@@ -356,6 +356,7 @@ struct btd_plan {
     int count = 0;
     const int64_t *c_idx = nullptr, *z_idx = nullptr, *e_idx = nullptr, *xl_idx = nullptr,
                   *h_idx = nullptr, *xh_idx = nullptr;
+    const int64_t *e_k = nullptr, *h_k = nullptr;  // 0 where the correction block is zero
     SplitK split;
   };
   int64_t partial_elems_per_k = 0;  // split-K scratch: doubles per unit K
@@ -364,6 +365,14 @@ struct btd_plan {
   // interface-RHS carry (local ranges whose last interior row exists)
   int ncarry = 0;
   const int64_t *carry_src = nullptr, *carry_fc = nullptr, *carry_row = nullptr;
+  // sharded: carry of the last owned range (sent to the next rank)
+  int ncarry_out = 0;
+  const int64_t *cout_fc = nullptr, *cout_row = nullptr;
+  // sharded: tree nodes whose segment crosses a rank boundary and that some rank needs;
+  // this rank contributes partial series sums over its own ranges
+  int ncross = 0;
+  const int64_t *cross_node = nullptr, *cross_roff = nullptr, *cross_ld = nullptr, *cross_k = nullptr,
+                *cross_lo = nullptr;
   // mode-1 per-step batches (local ranges)
   struct Step1 {
     int cnt = 0;
@@ -870,13 +879,20 @@ void build_local(btd_plan& pl, const double* diag, const double* lower, const do
   // ---- solve-time local batches
   {
     // carry_q = Fc_q y_{q,last}: ranges whose last interior row lies inside [0, n)
-    std::vector<int64_t> cs, cf, cr;
+    std::vector<int64_t> cs, cf, cr, of, orow;
     for (int64_t q = 0; q < nrl; ++q)
       if (cap > 0 && pl.nint[q] == cap && (pl.q0 + q + 1) * L <= n && pl.q0 + q + 1 < nr) {
-        cs.push_back(q); cf.push_back(pl.off_Fc + q); cr.push_back(pl.lo[q] + L - 1);
+        if (q + 1 < nrl) {
+          cs.push_back(q); cf.push_back(pl.off_Fc + q); cr.push_back(pl.lo[q] + L - 1);
+        } else {  // the next range belongs to the next rank
+          of.push_back(pl.off_Fc + q); orow.push_back(pl.lo[q] + L - 1);
+        }
       }
     pl.ncarry = (int)cs.size();
     pl.carry_src = pl.upload(cs); pl.carry_fc = pl.upload(cf); pl.carry_row = pl.upload(cr);
+    pl.ncarry_out = (int)of.size();
+    pl.cout_fc = pl.upload(of); pl.cout_row = pl.upload(orow);
+    if (pl.world == 1 && pl.ncarry_out) fail(BTD_ERR_CUDA, "internal: boundary carry on a single-rank plan");
     if (pl.mode == 1) {
       pl.steps1.resize(cap);
       for (int64_t j = 0; j < cap; ++j) {
@@ -1118,41 +1134,74 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
   }
   {  // solve-time batches over the nodes this rank needs
     // x~ needed for own interfaces q0..q1-1 and the right neighbour q1; node k needs x~_{lo-1}, x~_{hi+1}
-    std::vector<char> need_k(nr + 1, 0);
-    for (int64_t q = pl.q0; q <= std::min(pl.q1, nr - 1); ++q) need_k[q] = 1;
-    std::vector<int> node_of_k(nr, -1);
-    for (int b = 0; b < nn; ++b) node_of_k[pl.nodes[b].k] = b;
-    for (bool changed = true; changed;) {
-      changed = false;
-      for (int b = nn - 1; b >= 0; --b) {
-        const Node& nd = pl.nodes[b];
-        if (!need_k[nd.k]) continue;
-        if (nd.lo >= 1 && !need_k[nd.lo - 1]) { need_k[nd.lo - 1] = 1; changed = true; }
-        if (nd.hi + 1 <= nr - 1 && !need_k[nd.hi + 1]) { need_k[nd.hi + 1] = 1; changed = true; }
+    auto needed = [&](int64_t q0, int64_t q1) {
+      std::vector<char> need(nr + 1, 0);
+      for (int64_t q = q0; q <= std::min(q1, nr - 1); ++q) need[q] = 1;
+      for (bool changed = true; changed;) {
+        changed = false;
+        for (int b = nn - 1; b >= 0; --b) {
+          const Node& nd = pl.nodes[b];
+          if (!need[nd.k]) continue;
+          if (nd.lo >= 1 && !need[nd.lo - 1]) { need[nd.lo - 1] = 1; changed = true; }
+          if (nd.hi + 1 <= nr - 1 && !need[nd.hi + 1]) { need[nd.hi + 1] = 1; changed = true; }
+        }
+      }
+      return need;
+    };
+    const std::vector<char> need_k = needed(pl.q0, pl.q1);
+    // crossing nodes: needed by some rank, segment not inside that rank's ranges (same list on every rank)
+    std::vector<char> crossing(nn, 0);
+    if (pl.world > 1) {
+      for (int r = 0; r < pl.world; ++r) {
+        const int64_t a0 = r * pl.nrl, a1 = (r + 1) * pl.nrl;
+        const std::vector<char> nr_ = needed(a0, a1);
+        for (int b = 0; b < nn; ++b)
+          if (nr_[pl.nodes[b].k] && (pl.nodes[b].lo < a0 || pl.nodes[b].hi >= a1)) crossing[b] = 1;
       }
     }
     std::vector<int64_t> zid, zro, zrl, znl;
     for (int b = 0; b < nn; ++b)
-      if (need_k[pl.nodes[b].k]) { zid.push_back(b); zro.push_back(roff[b]); zrl.push_back(rld[b]); znl.push_back(pl.nodes[b].lo); }
+      if (need_k[pl.nodes[b].k] && !crossing[b]) {
+        zid.push_back(b); zro.push_back(roff[b]); zrl.push_back(rld[b]); znl.push_back(pl.nodes[b].lo);
+      }
     pl.nz = (int)zid.size();
     pl.z_id = pl.upload(zid); pl.z_roff = pl.upload(zro); pl.z_rld = pl.upload(zrl); pl.z_nlo = pl.upload(znl);
+    std::vector<int64_t> cn, cro, cld, ck, clo;
+    for (int b = 0; b < nn; ++b) {
+      if (!crossing[b]) continue;
+      const Node& nd = pl.nodes[b];
+      const int64_t a = std::max(nd.lo, pl.q0), e = std::min(nd.hi, pl.q1 - 1);
+      cn.push_back(b);
+      cld.push_back(rld[b]);
+      if (a <= e) {
+        cro.push_back(roff[b] + (a - nd.lo) * mp); ck.push_back((e - a + 1) * mp); clo.push_back(a);
+      } else {
+        cro.push_back(roff[b]); ck.push_back(0); clo.push_back(0);
+      }
+    }
+    pl.ncross = (int)cn.size();
+    pl.cross_node = pl.upload(cn); pl.cross_roff = pl.upload(cro); pl.cross_ld = pl.upload(cld);
+    pl.cross_k = pl.upload(ck); pl.cross_lo = pl.upload(clo);
     std::vector<int64_t> nlo(nn);
     for (int b = 0; b < nn; ++b) nlo[b] = pl.nodes[b].lo;
     pl.d_nlo = pl.upload(nlo);
     pl.levels.assign(maxlevel + 1, btd_plan::Level());
     for (int64_t lev = 0; lev <= maxlevel; ++lev) {
-      std::vector<int64_t> c, z, e, xl, h, xh;
+      std::vector<int64_t> c, z, e, xl, h, xh, ek, hk;
       for (int b = 0; b < nn; ++b) {
         const Node& nd = pl.nodes[b];
         if (nd.level != lev || !need_k[nd.k]) continue;
         c.push_back(nd.k); z.push_back(b); e.push_back(2 * b); h.push_back(2 * b + 1);
         xl.push_back(nd.lo >= 1 ? nd.lo - 1 : nr);
         xh.push_back(nd.hi + 1 <= nr - 1 ? nd.hi + 1 : nr);
+        ek.push_back(nd.lo >= 1 ? mp : 0);
+        hk.push_back(nd.hi + 1 <= nr - 1 ? mp : 0);
       }
       auto& L_ = pl.levels[lev];
       L_.count = (int)c.size();
       L_.c_idx = pl.upload(c); L_.z_idx = pl.upload(z); L_.e_idx = pl.upload(e);
       L_.xl_idx = pl.upload(xl); L_.h_idx = pl.upload(h); L_.xh_idx = pl.upload(xh);
+      L_.e_k = pl.upload(ek); L_.h_k = pl.upload(hk);
     }
     // split-K plans: enough CTAs (>= 2 waves) for the series sums and the level corrections
     pl.z_k = zrl;
@@ -1233,20 +1282,26 @@ void solve_forward(btd_plan& pl, const double* F, double* X, int64_t K, double* 
   }
 }
 
-// Algorithm 1 on the interface system: z = R f~ (all nodes), then the levels.
-void solve_tree(btd_plan& pl, int64_t K, cudaStream_t st) {
+// Algorithm 1, level part: x~_k = z_node + E x~_{lo-1} + H x~_{hi+1}, level by level.
+void solve_levels(btd_plan& pl, int64_t K, cudaStream_t st) {
   const int64_t mp = pl.mp, blk = pl.blk, mpK = mp * K;
-  double* ft = pl.ft.d();
   double* xt = pl.xt.d();
   double* z = pl.zbuf.d();
-  launch_gemm(mp, K, pl.nz, mk(z, pl.z_id, 0, mpK, K), none(), 0.0,
-              {term(mk(pl.Rrows.d(), pl.z_roff, 0, 1, 0, pl.z_rld), mk(ft, pl.z_nlo, 0, mpK, K), 0, 1.0, pl.z_rld)}, st,
-              &pl.z_split);
   for (const auto& lev : pl.levels)
     launch_gemm(mp, K, lev.count, mk(xt, lev.c_idx, 0, mpK, K), mk(z, lev.z_idx, 0, mpK, K), 1.0,
-                {term(mk(pl.EH.d(), lev.e_idx, 0, blk, mp), mk(xt, lev.xl_idx, 0, mpK, K), mp),
-                 term(mk(pl.EH.d(), lev.h_idx, 0, blk, mp), mk(xt, lev.xh_idx, 0, mpK, K), mp)},
+                {term(mk(pl.EH.d(), lev.e_idx, 0, blk, mp), mk(xt, lev.xl_idx, 0, mpK, K), mp, 1.0, lev.e_k),
+                 term(mk(pl.EH.d(), lev.h_idx, 0, blk, mp), mk(xt, lev.xh_idx, 0, mpK, K), mp, 1.0, lev.h_k)},
                 st, &lev.split);
+}
+
+// Algorithm 1 on the interface system: z = R f~ (all needed nodes), then the levels.
+void solve_tree(btd_plan& pl, int64_t K, cudaStream_t st) {
+  const int64_t mp = pl.mp, mpK = mp * K;
+  launch_gemm(mp, K, pl.nz, mk(pl.zbuf.d(), pl.z_id, 0, mpK, K), none(), 0.0,
+              {term(mk(pl.Rrows.d(), pl.z_roff, 0, 1, 0, pl.z_rld), mk(pl.ft.d(), pl.z_nlo, 0, mpK, K), 0, 1.0,
+                    pl.z_rld)},
+              st, &pl.z_split);
+  solve_levels(pl, K, st);
 }
 
 // Backward sweeps of the owned ranges (x~ known), x[lo_q] = x~_q.
@@ -1347,23 +1402,66 @@ void solve_graphed(btd_plan& pl, const double* F, double* X, int64_t K, cudaStre
   CK(cudaStreamWaitEvent(st, pl.ev_out, 0));
 }
 
-// Sharded phase A: local sweeps, then this rank's (base, carry) pairs into exch [nrl][2][mp][K].
-void solve_shard_a(btd_plan& pl, const double* F, double* X, int64_t K, double* exch, cudaStream_t st) {
+// Sharded phase A: local sweeps (base into f~), internal carries, and the carry of
+// the last owned range for the next rank (carry_out: mp x K, zero if none).
+void solve_shard_a(btd_plan& pl, const double* F, double* X, int64_t K, double* carry_out, cudaStream_t st) {
   const int64_t mp = pl.mp, m = pl.m, blk = pl.blk, mpK = mp * K, mK = m * K;
-  CK(cudaMemsetAsync(exch, 0, (size_t)pl.nrl * 2 * mpK * sizeof(double), st));
+  double* ft = pl.ft.d() + pl.q0 * mpK;
+  CK(cudaMemsetAsync(carry_out, 0, (size_t)mpK * sizeof(double), st));
   pl.ev_mark(st);
-  solve_forward(pl, F, X, K, exch, 2 * mpK, st);
+  solve_forward(pl, F, X, K, ft, mpK, st);
   pl.ev_mark(st);
-  launch_gemm(mp, K, pl.ncarry, mk(exch + mpK, pl.carry_src, 0, 2 * mpK, K), none(), 0.0,
+  launch_gemm(mp, K, pl.ncarry, mk(ft, pl.carry_src, 1, mpK, K), mk(ft, pl.carry_src, 1, mpK, K), 1.0,
               {term(mk(pl.pool.d(), pl.carry_fc, 0, blk, mp), mk(X, pl.carry_row, 0, mK, K), m)}, st);
+  launch_gemm(mp, K, pl.ncarry_out, mk(carry_out, nullptr, 0, mpK, K), none(), 0.0,
+              {term(mk(pl.pool.d(), pl.cout_fc, 0, blk, mp), mk(X, pl.cout_row, 0, mK, K), m)}, st);
 }
 
-// Sharded phase B: interface RHS from the all-gathered pairs, tree, local recovery.
-void solve_shard_b(btd_plan& pl, const double* exch_all, const double* F, double* X, int64_t K, cudaStream_t st) {
-  const int64_t mpK = pl.mp * K;
-  assemble_ft_kernel<<<592, 256, 0, st>>>(exch_all, pl.ft.d(), pl.nr, mpK);
-  CK_LAUNCH();
-  solve_tree(pl, K, st);
+__global__ void add_block_kernel(double* dst, const double* src, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] += src[e];
+}
+
+// z_b = sum over ranks (fixed order) of the partial series sums of crossing node c
+__global__ void sum_ranks_kernel(const double* part_all, int world, int ncross, int64_t per, const int64_t* node,
+                                 double* z) {
+  for (int c = blockIdx.y; c < ncross; c += gridDim.y) {
+    double* zb = z + node[c] * per;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per; e += (int64_t)gridDim.x * blockDim.x) {
+      double v = 0.0;
+      for (int r = 0; r < world; ++r) v += part_all[((int64_t)r * ncross + c) * per + e];
+      zb[e] = v;
+    }
+  }
+}
+
+// Sharded phase B: finish f~ of the first owned range with the previous rank's carry,
+// local series sums of nodes inside this rank, partial sums of crossing nodes.
+void solve_shard_b(btd_plan& pl, const double* carry_all, double* partial_out, int64_t K, cudaStream_t st) {
+  const int64_t mp = pl.mp, mpK = mp * K;
+  double* ft = pl.ft.d();
+  if (pl.rank >= 1) {
+    add_block_kernel<<<64, 256, 0, st>>>(ft + pl.q0 * mpK, carry_all + (int64_t)(pl.rank - 1) * mpK, mpK);
+    CK_LAUNCH();
+  }
+  launch_gemm(mp, K, pl.nz, mk(pl.zbuf.d(), pl.z_id, 0, mpK, K), none(), 0.0,
+              {term(mk(pl.Rrows.d(), pl.z_roff, 0, 1, 0, pl.z_rld), mk(ft, pl.z_nlo, 0, mpK, K), 0, 1.0, pl.z_rld)}, st,
+              &pl.z_split);
+  launch_gemm(mp, K, pl.ncross, mk(partial_out, nullptr, 0, mpK, K), none(), 0.0,
+              {term(mk(pl.Rrows.d(), pl.cross_roff, 0, 1, 0, pl.cross_ld), mk(ft, pl.cross_lo, 0, mpK, K), 0, 1.0,
+                    pl.cross_k)},
+              st);
+}
+
+// Sharded phase C: crossing-node sums, tree levels, local recovery.
+void solve_shard_c(btd_plan& pl, const double* partial_all, const double* F, double* X, int64_t K, cudaStream_t st) {
+  const int64_t mp = pl.mp, mpK = mp * K;
+  if (pl.ncross) {
+    dim3 grid((unsigned)std::min<int64_t>((mpK + 255) / 256, 64), (unsigned)std::min(pl.ncross, 65535));
+    sum_ranks_kernel<<<grid, 256, 0, st>>>(partial_all, pl.world, pl.ncross, mpK, pl.cross_node, pl.zbuf.d());
+    CK_LAUNCH();
+  }
+  solve_levels(pl, K, st);
   pl.ev_mark(st);
   solve_backward(pl, F, X, K, st);
   pl.ev_mark(st);
@@ -1467,40 +1565,52 @@ int btd_shard_finish(btd_plan* pl, const double* contrib_all, void* stream, int6
   return rc;
 }
 
-int btd_shard_exchange_size(const btd_plan* pl, int64_t k, int64_t* nelems_local) {
-  if (!pl || !nelems_local) return BTD_ERR_INVALID_ARG;
-  *nelems_local = pl->nrl * 2 * pl->mp * k;
+int btd_shard_exchange_size(const btd_plan* pl, int64_t k, int64_t* n_carry, int64_t* n_partial) {
+  if (!pl || !n_carry || !n_partial) return BTD_ERR_INVALID_ARG;
+  *n_carry = pl->mp * k;
+  *n_partial = (int64_t)pl->ncross * pl->mp * k;
   return BTD_OK;
 }
 
-int btd_shard_solve_a(btd_plan* pl, const double* f_local, double* x_local, int64_t k, double* exch_local,
+int btd_shard_solve_a(btd_plan* pl, const double* f_local, double* x_local, int64_t k, double* carry_out,
                       void* stream) {
-  if (!pl || !pl->finished || (pl->nloc > 0 && (!f_local || !x_local)) || !exch_local || k < 1) {
+  if (!pl || !pl->finished || (pl->nloc > 0 && (!f_local || !x_local)) || !carry_out || k < 1) {
     g_err = "btd_shard_solve_a: bad argument or unfinished plan";
     return BTD_ERR_INVALID_ARG;
   }
   return guarded(pl, stream, [&](cudaStream_t st) {
     ensure_scratch(*pl, k);
-    solve_shard_a(*pl, f_local, x_local, k, exch_local, st);
+    solve_shard_a(*pl, f_local, x_local, k, carry_out, st);
   });
 }
 
-int btd_shard_solve_b(btd_plan* pl, const double* exch_all, const double* f_local, double* x_local, int64_t k,
-                      void* stream) {
-  if (!pl || !pl->finished || !exch_all || (pl->nloc > 0 && !x_local) || k < 1) {
+int btd_shard_solve_b(btd_plan* pl, const double* carry_all, double* partial_out, int64_t k, void* stream) {
+  if (!pl || !pl->finished || !carry_all || (pl->ncross && !partial_out) || k < 1) {
     g_err = "btd_shard_solve_b: bad argument or unfinished plan";
     return BTD_ERR_INVALID_ARG;
   }
   return guarded(pl, stream, [&](cudaStream_t st) {
     ensure_scratch(*pl, k);
-    solve_shard_b(*pl, exch_all, f_local, x_local, k, st);
+    solve_shard_b(*pl, carry_all, partial_out, k, st);
+  });
+}
+
+int btd_shard_solve_c(btd_plan* pl, const double* partial_all, const double* f_local, double* x_local, int64_t k,
+                      void* stream) {
+  if (!pl || !pl->finished || (pl->ncross && !partial_all) || (pl->nloc > 0 && !x_local) || k < 1) {
+    g_err = "btd_shard_solve_c: bad argument or unfinished plan";
+    return BTD_ERR_INVALID_ARG;
+  }
+  return guarded(pl, stream, [&](cudaStream_t st) {
+    ensure_scratch(*pl, k);
+    solve_shard_c(*pl, partial_all, f_local, x_local, k, st);
   });
 }
 
 int btd_plan_solve(btd_plan* pl, const double* f, double* x, int64_t k, void* stream) {
   if (!pl || !f || !x) { g_err = "NULL argument"; return BTD_ERR_INVALID_ARG; }
   if (k < 1) { g_err = "k must be >= 1"; return BTD_ERR_DIMENSION; }
-  if (pl->world != 1) { g_err = "sharded plan: use btd_shard_solve_a/b"; return BTD_ERR_INVALID_ARG; }
+  if (pl->world != 1) { g_err = "sharded plan: use btd_shard_solve_a/b/c"; return BTD_ERR_INVALID_ARG; }
   return guarded(pl, stream, [&](cudaStream_t st) {
     ensure_scratch(*pl, k);
     solve_graphed(*pl, f, x, k, st);
@@ -1510,7 +1620,7 @@ int btd_plan_solve(btd_plan* pl, const double* f, double* x, int64_t k, void* st
 int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int64_t k, void* stream) {
   if (!pl || !f_host || !x_host) { g_err = "NULL argument"; return BTD_ERR_INVALID_ARG; }
   if (k < 1) { g_err = "k must be >= 1"; return BTD_ERR_DIMENSION; }
-  if (pl->world != 1) { g_err = "sharded plan: use btd_shard_solve_a/b"; return BTD_ERR_INVALID_ARG; }
+  if (pl->world != 1) { g_err = "sharded plan: use btd_shard_solve_a/b/c"; return BTD_ERR_INVALID_ARG; }
   return guarded(pl, stream, [&](cudaStream_t st) {
     const size_t bytes = (size_t)pl->n * pl->m * k * sizeof(double);
     if (pl->hostio_k != k) {

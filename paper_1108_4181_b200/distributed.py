@@ -10,9 +10,15 @@ the ranks are real processes, one B200 each:
   emits four reduced-system contributions per range; one NCCL all-gather of
   those (4 M^2 doubles per range; the paper's step 1.2) lets every rank
   assemble the reduced system and its partition-tree inverse rows;
-* solve: phase A (local fused sweeps) -> one NCCL all-gather of the (base,
-  carry) pairs (2 M K doubles per range, the reference's exchange) ->
-  phase B (interface RHS, tree solve, local recovery).
+* solve: phase A (local fused sweeps) -> NCCL all-gather of one carry block
+  per rank (the coupling into the next rank's first interface) -> phase B
+  (interface RHS of the own ranges; partial series sums R_node f~ over the own
+  ranges for the tree nodes whose segment crosses a rank boundary) -> NCCL
+  all-gather of those partials, summed in rank order (deterministic) ->
+  phase C (tree levels for the nodes this rank needs, local recovery).  This
+  is the paper's "sum of a series over distributed data": M K (1 + #crossing
+  nodes) doubles per rank per solve instead of the reference harness's
+  all-gather of every range's (base, carry) pair.
 
 On NVSwitch a single all-gather replaces the dissemination rounds; the stage
 law (ceil(log2 p) logical stages) is reported by :func:`stage_count`.
@@ -97,18 +103,22 @@ class NativeBackend:
         return self.torch.empty(nel, dtype=self.torch.float64, device=f"cuda:{self.device}")
 
     def exchange_size(self, h, k):
-        nel = ctypes.c_int64()
-        _native.check(self.lib.btd_shard_exchange_size(h, k, ctypes.byref(nel)))
-        return nel.value
+        nc, npart = ctypes.c_int64(), ctypes.c_int64()
+        _native.check(self.lib.btd_shard_exchange_size(h, k, ctypes.byref(nc), ctypes.byref(npart)))
+        return nc.value, npart.value
 
-    def solve_a(self, h, f_local, x_local, k, exch):
+    def solve_a(self, h, f_local, x_local, k, carry):
         with self.torch.cuda.device(self.device):
-            _native.check(self.lib.btd_shard_solve_a(h, self._p(f_local), self._p(x_local), k, self._p(exch),
+            _native.check(self.lib.btd_shard_solve_a(h, self._p(f_local), self._p(x_local), k, self._p(carry),
                                                      self._stream()))
 
-    def solve_b(self, h, exch_all, f_local, x_local, k):
+    def solve_b(self, h, carry_all, partial, k):
         with self.torch.cuda.device(self.device):
-            _native.check(self.lib.btd_shard_solve_b(h, self._p(exch_all), self._p(f_local), self._p(x_local), k,
+            _native.check(self.lib.btd_shard_solve_b(h, self._p(carry_all), self._p(partial), k, self._stream()))
+
+    def solve_c(self, h, partial_all, f_local, x_local, k):
+        with self.torch.cuda.device(self.device):
+            _native.check(self.lib.btd_shard_solve_c(h, self._p(partial_all), self._p(f_local), self._p(x_local), k,
                                                      self._stream()))
 
     def destroy(self, h):
@@ -181,12 +191,17 @@ class ShardedPlan:
         (written into ``out`` when given; may alias f_local)."""
         k = int(f_local.shape[2])
         x_local = f_local.new_empty(f_local.shape) if out is None else out
-        nel = self.be.exchange_size(self.h, k)
-        exch = self.be.empty(nel)
-        self.be.solve_a(self.h, f_local, x_local, k, exch)
-        allx = self.be.empty(nel * self.world)
-        self.dist.all_gather_into_tensor(allx, exch, group=self.group)
-        self.be.solve_b(self.h, allx, f_local, x_local, k)
+        nc, npart = self.be.exchange_size(self.h, k)
+        carry = self.be.empty(nc)
+        self.be.solve_a(self.h, f_local, x_local, k, carry)
+        carry_all = self.be.empty(nc * self.world)
+        self.dist.all_gather_into_tensor(carry_all, carry, group=self.group)
+        part = self.be.empty(max(npart, 1))
+        self.be.solve_b(self.h, carry_all, part, k)
+        part_all = self.be.empty(max(npart, 1) * self.world)
+        if npart:
+            self.dist.all_gather_into_tensor(part_all, part[:npart], group=self.group)
+        self.be.solve_c(self.h, part_all, f_local, x_local, k)
         return x_local
 
     def close(self):

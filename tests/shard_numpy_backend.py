@@ -102,12 +102,13 @@ class NumpyShardBackend:
         return 0, -1
 
     def exchange_size(self, h, k):
-        return h.nrl * 2 * h.m * k
+        # carry block; "partials" = this rank's f~ slices embedded in a global array
+        return h.m * k, h.nr * h.m * k
 
-    def solve_a(self, h, f_local, x_local, k, exch):
+    def solve_a(self, h, f_local, x_local, k, carry):
         f, x = f_local.numpy(), x_local.numpy()
-        ex = np.zeros((h.nrl, 2, h.m, k))
-        h.y = []
+        h.base = np.zeros((h.nrl, h.m, k))
+        h.carries = np.zeros((h.nrl, h.m, k))
         for ql, F in enumerate(h.fac):
             lo = ql * h.L
             base = f[lo].copy() if lo < h.nloc else np.zeros((h.m, k))
@@ -116,16 +117,27 @@ class NumpyShardBackend:
                 y = F["Dinv"][j] @ f[lo + 1 + j] + (F["AD"][j] @ y if j else 0)
                 x[lo + 1 + j] = y
                 base += F["Tb"][j] @ y
-            ex[ql, 0] = base
+            h.base[ql] = base
             if F["nint"] == h.L - 1 and h.L >= 2 and h.q0 + ql + 1 < h.nr and (h.q0 + ql + 1) * h.L <= h.n:
-                ex[ql, 1] = F["Fc"] @ x[lo + h.L - 1]
-        exch.copy_(torch.from_numpy(ex.reshape(-1)))
+                h.carries[ql] = F["Fc"] @ x[lo + h.L - 1]
+        carry.copy_(torch.from_numpy(h.carries[-1].reshape(-1).copy()))
 
-    def solve_b(self, h, exch_all, f_local, x_local, k):
+    def solve_b(self, h, carry_all, partial, k):
+        ca = carry_all.numpy().reshape(h.world, h.m, k)
+        ft = h.base.copy()
+        ft[1:] += h.carries[:-1]
+        if h.q0 > 0:
+            ft[0] += ca[h.q0 // h.nrl - 1]
+        glob = np.zeros((h.nr, h.m, k))
+        glob[h.q0:h.q0 + h.nrl] = ft
+        partial.copy_(torch.from_numpy(glob.reshape(-1)))
+
+    def solve_c(self, h, partial_all, f_local, x_local, k):
         x = x_local.numpy()
-        ex = exch_all.numpy().reshape(h.nr, 2, h.m, k)
-        ft = ex[:, 0].copy()
-        ft[1:] += ex[:-1, 1]
+        parts = partial_all.numpy().reshape(h.world, h.nr, h.m, k)
+        ft = parts[0].copy()
+        for r in range(1, h.world):
+            ft += parts[r]
         xt = np.linalg.solve(h.R, ft.reshape(h.nr * h.m, k)).reshape(h.nr, h.m, k)
         xt = np.concatenate([xt, np.zeros((1, h.m, k))])
         for ql, F in enumerate(h.fac):

@@ -37,17 +37,24 @@ def _emulate(d, lo, up, f, ranks, split, world):
     infos = [be.info(h) for h in hs]
     k = f.shape[2]
     ft = torch.from_numpy(f).cuda()
-    xs, exs = [], []
+    xs, carries, parts = [], [], []
     for h, inf in zip(hs, infos):
         fl = ft[inf.row_lo:inf.row_hi].contiguous()
         xl = torch.empty_like(fl)
-        ex = be.empty(be.exchange_size(h, k))
-        be.solve_a(h, fl, xl, k, ex)
+        nc, npart = be.exchange_size(h, k)
+        c = be.empty(nc)
+        be.solve_a(h, fl, xl, k, c)
         xs.append((fl, xl))
-        exs.append(ex)
-    allx = torch.cat(exs)
+        carries.append(c)
+    carry_all = torch.cat(carries)
+    for h in hs:
+        nc, npart = be.exchange_size(h, k)
+        pt = be.empty(max(npart, 1))
+        be.solve_b(h, carry_all, pt, k)
+        parts.append(pt[:npart])
+    part_all = torch.cat(parts) if parts[0].numel() else be.empty(1)
     for h, (fl, xl) in zip(hs, xs):
-        be.solve_b(h, allx, fl, xl, k)
+        be.solve_c(h, part_all, fl, xl, k)
     torch.cuda.synchronize()
     x = torch.cat([xl for _, xl in xs]).cpu().numpy()
     for h in hs:
