@@ -53,7 +53,7 @@ BENCH_CFG = {
     # c3: the explicit interface Schur complement S (N=63, M=2048) of the 64-subdomain
     # Helmholtz DD; P = 9 ranges of 7 interface rows on one GPU (288 GEMM tiles fill the
     # 296 CTA slots), P = 8 (a multiple of 2/4/8) when sharded
-    "c3": dict(subdomains_per_gpu=lambda w: 9 if w == 1 else 8 // w, ranges_per_gpu=8),
+    "c3": dict(subdomains_per_gpu=lambda w: 9 if w == 1 else 8 // w, ranges_per_gpu=1),
     "c4": dict(subdomains_per_gpu=lambda w: 8 * w, ranges_per_gpu=592),
 }
 
