@@ -418,7 +418,8 @@ def run_b200(args):
         roof = {"bound": "tensor", "achieved": fwd_flops / t_fwd / 1e12, "peak": fp64, "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = ncu_traffic(name)
-    roof["kernel"] = "chain_fwd_kernel" if mode == 0 else "gemm_batched_kernel (mode 1)"
+    roof["kernel"] = (("stream_fwd_kernel (TMA bulk-copy ring)" if m <= 32 and K % 2 == 0 else "chain_fwd_kernel")
+                      if mode == 0 else "gemm_pipe_kernel (mode 1: one batched GEMM per row step)")
     roof["peak_source"] = ("cuBLAS DGEMM 4096^3 measured in this run (fp64 tensor; MEASURED_PEAKS.json has no fp64)"
                            if not hbm_bound else "MEASURED_PEAKS.json hbm_gbs")
     t_roof = max(tot_flops / (fp64 * 1e12), tot_bytes / (hbm * 1e9))

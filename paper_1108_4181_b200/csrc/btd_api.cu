@@ -400,6 +400,11 @@ struct btd_plan {
   };
   std::vector<GraphEntry> graphs;
   cudaStream_t own = nullptr;
+  // pipelined host path: copy-in / copy-out streams, double-buffered column chunks
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_h[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  DevBuf hchunk[2];
+  int64_t hchunk_elems = 0;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   // cuSOLVER for block orders above 256 (preprocessing only)
   cusolverDnHandle_t solver = nullptr;
@@ -440,6 +445,11 @@ struct btd_plan {
     for (auto& g : graphs)
       if (g.exec) cudaGraphExecDestroy(g.exec);
     if (own) cudaStreamDestroy(own);
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
+    for (auto& a : ev_h)
+      for (auto& e : a)
+        if (e) cudaEventDestroy(e);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
   }
@@ -1617,24 +1627,65 @@ int btd_plan_solve(btd_plan* pl, const double* f, double* x, int64_t k, void* st
   });
 }
 
+// Host-memory solve (the reference's numpy-in / numpy-out contract).  Columns are
+// independent, so the K columns run as equal chunks through a 3-stream pipeline:
+// H2D of chunk c+1 (2-D strided copy out of the (n, m, k) layout) || solve of chunk c
+// || D2H of chunk c-1, with two device chunk buffers.  Needs pinned host memory to
+// overlap (pageable memory still works, synchronously).
 int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int64_t k, void* stream) {
   if (!pl || !f_host || !x_host) { g_err = "NULL argument"; return BTD_ERR_INVALID_ARG; }
   if (k < 1) { g_err = "k must be >= 1"; return BTD_ERR_DIMENSION; }
   if (pl->world != 1) { g_err = "sharded plan: use btd_shard_solve_a/b/c"; return BTD_ERR_INVALID_ARG; }
   return guarded(pl, stream, [&](cudaStream_t st) {
-    const size_t bytes = (size_t)pl->n * pl->m * k * sizeof(double);
-    if (pl->hostio_k != k) {
+    // chunk width: an even divisor of k giving up to 4 chunks of >= 32 columns (>= 256 B rows)
+    int64_t kc = k;
+    for (int64_t nch : {4, 2})
+      if (k % nch == 0 && (k / nch) % 2 == 0 && k / nch >= 32) { kc = k / nch; break; }
+    const int64_t nch = k / kc, rows = pl->n * pl->m;
+    const size_t celems = (size_t)rows * kc;
+    if (pl->hostio_k != kc) {
       for (auto& g : pl->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
       pl->graphs.clear();
-      pl->hostio.alloc(bytes);
-      pl->hostio_k = k;
+      pl->hostio_k = kc;
     }
-    ensure_scratch(*pl, k);
-    CK(cudaMemcpyAsync(pl->hostio.p, f_host, bytes, cudaMemcpyHostToDevice, st));
-    solve_graphed(*pl, pl->hostio.d(), pl->hostio.d(), k, st);
-    CK(cudaMemcpyAsync(x_host, pl->hostio.p, bytes, cudaMemcpyDeviceToHost, st));
+    if ((int64_t)celems > pl->hchunk_elems) {
+      pl->hchunk[0].alloc(celems * sizeof(double));
+      pl->hchunk[1].alloc(celems * sizeof(double));
+      pl->hchunk_elems = (int64_t)celems;
+      for (auto& g : pl->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+      pl->graphs.clear();
+    }
+    if (!pl->s_in) {
+      CK(cudaStreamCreateWithFlags(&pl->s_in, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&pl->s_out, cudaStreamNonBlocking));
+      for (auto& a : pl->ev_h)
+        for (auto& e : a) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    ensure_scratch(*pl, kc);
+    cudaEvent_t start;
+    CK(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    CK(cudaEventRecord(start, st));
+    CK(cudaStreamWaitEvent(pl->s_in, start, 0));
+    const size_t wbytes = (size_t)kc * sizeof(double), hpitch = (size_t)k * sizeof(double);
+    for (int64_t c = 0; c < nch; ++c) {
+      const int b = (int)(c & 1);
+      double* dbuf = pl->hchunk[b].d();
+      cudaEvent_t in_done = pl->ev_h[b][0], comp_done = pl->ev_h[b][1], out_done = pl->ev_h[b][2];
+      if (c >= 2) CK(cudaStreamWaitEvent(pl->s_in, out_done, 0));  // buffer b free again
+      CK(cudaMemcpy2DAsync(dbuf, wbytes, f_host + c * kc, hpitch, wbytes, rows, cudaMemcpyHostToDevice, pl->s_in));
+      CK(cudaEventRecord(in_done, pl->s_in));
+      CK(cudaStreamWaitEvent(st, in_done, 0));
+      solve_graphed(*pl, dbuf, dbuf, kc, st);
+      CK(cudaEventRecord(comp_done, st));
+      CK(cudaStreamWaitEvent(pl->s_out, comp_done, 0));
+      CK(cudaMemcpy2DAsync(x_host + c * kc, hpitch, dbuf, wbytes, wbytes, rows, cudaMemcpyDeviceToHost, pl->s_out));
+      CK(cudaEventRecord(out_done, pl->s_out));
+    }
+    CK(cudaStreamSynchronize(pl->s_out));
     CK(cudaStreamSynchronize(st));
+    cudaEventDestroy(start);
   });
 }
 
