@@ -543,14 +543,15 @@ __global__ void __launch_bounds__(32 * WR * WC) chain_bwd_kernel(ChainArgs a) {
 // cp.async.bulk (TMA) and completed on an mbarrier; NSTG rows are in flight.
 template <int MP, int NW, int NSTG>
 struct StreamCfg {
-  static constexpr int KC = 16 * NW, LDT = KC + 2, NT = 32 * NW;
+  static constexpr int KC = 16 * NW, LDT = KC + 2;
+  static constexpr int NT = 32 * (NW + 1);  // NW consumer warps + 1 producer warp
   static constexpr int TM = MP / 8, TN = 2, NSP = MP / 8;
   static constexpr int BLK = MP * MP;
   static constexpr int TILE = MP * LDT;
   static constexpr int FWD_STAGE = TILE + 3 * BLK;  // F tile + AD, Tb, Dinv
   static constexpr int BWD_STAGE = TILE + 2 * BLK;  // y tile + G, S
-  static constexpr size_t FWD_SMEM = (size_t)(TILE + NSTG * FWD_STAGE) * 8 + NSTG * 8;
-  static constexpr size_t BWD_SMEM = (size_t)(2 * TILE + NSTG * BWD_STAGE) * 8 + NSTG * 8;
+  static constexpr size_t FWD_SMEM = (size_t)(TILE + NSTG * FWD_STAGE) * 8 + 2 * NSTG * 8;
+  static constexpr size_t BWD_SMEM = (size_t)(2 * TILE + NSTG * BWD_STAGE) * 8 + 2 * NSTG * 8;
 };
 
 // acc += A(smem block, warp-all rows) @ B(smem tile, cols c0..c0+15)
@@ -587,24 +588,31 @@ BTD_DEVINL unsigned issue_tile(double* dst, int ldt, const double* src, int64_t 
   return rb * (unsigned)m;
 }
 
+// Warp-specialised streamed sweeps.  Warps split the CTA's columns, so a
+// consumer warp's slice of the chain state (y / x) depends on its own columns
+// only: no CTA barrier per row.  The producer warp refills ring slot s with row
+// r once every consumer warp has released it (empty[s], count NW).
 template <int MP, int NW, int NSTG>
-__global__ void __launch_bounds__(32 * NW) stream_fwd_kernel(ChainArgs a) {
+__global__ void __launch_bounds__(32 * (NW + 1)) stream_fwd_kernel(ChainArgs a) {
   using C = StreamCfg<MP, NW, NSTG>;
   constexpr int TM = C::TM, TN = C::TN, LDT = C::LDT;
   extern __shared__ __align__(16) double sm[];
   double* Ys = sm;
   double* stg = sm + C::TILE;
   uint64_t* full = reinterpret_cast<uint64_t*>(stg + NSTG * C::FWD_STAGE);
+  uint64_t* empty = full + NSTG;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int q = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * C::KC;
   const int64_t K = a.K;
   const int ncols = (int)(K - c0 < C::KC ? K - c0 : C::KC);
-  const int cw = warp * 16;
   for (int e = tid; e < C::TILE + NSTG * C::FWD_STAGE; e += C::NT) sm[e] = 0.0;
   if (tid == 0) {
-    for (int i = 0; i < NSTG; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < NSTG; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NW);
+    }
     mbar_fence_init();
   }
   __syncthreads();
@@ -614,51 +622,53 @@ __global__ void __launch_bounds__(32 * NW) stream_fwd_kernel(ChainArgs a) {
   const int64_t rowK = (int64_t)a.m * K;
   constexpr int64_t blk = C::BLK;
 
-  // producer (warp 0): stage for row j into slot j % NSTG
-  auto produce = [&](int j) {
-    double* st = stg + (j % NSTG) * C::FWD_STAGE;
-    uint64_t* bar = &full[j % NSTG];
-    fence_proxy_async();  // slot was read through the generic proxy
-    if (lane == 0) mbar_expect_tx(bar, (unsigned)(a.m * ncols * 8) + 3u * blk * 8u);
-    __syncwarp();
-    issue_tile(st, LDT, a.F + (lo + 1 + j) * rowK + c0, K, a.m, ncols, bar, lane);
-    if (lane == 0) {
-      const int64_t sl = slot0 + j;
-      bulk_g2s(st + C::TILE, a.AD + sl * blk, blk * 8, bar);
-      bulk_g2s(st + C::TILE + blk, a.Tb + (j > 0 ? sl - 1 : sl) * blk, blk * 8, bar);
-      bulk_g2s(st + C::TILE + 2 * blk, a.Dinv + sl * blk, blk * 8, bar);
+  if (warp == NW) {  // ---- producer
+    for (int j = 0; j < nint; ++j) {
+      const int sl = j % NSTG;
+      if (j >= NSTG) mbar_wait(&empty[sl], (unsigned)(((j / NSTG) - 1) & 1));
+      double* st = stg + sl * C::FWD_STAGE;
+      fence_proxy_async();
+      if (lane == 0) mbar_expect_tx(&full[sl], (unsigned)(a.m * ncols * 8) + 3u * blk * 8u);
+      __syncwarp();
+      issue_tile(st, LDT, a.F + (lo + 1 + j) * rowK + c0, K, a.m, ncols, &full[sl], lane);
+      if (lane == 0) {
+        const int64_t s_ = slot0 + j;
+        bulk_g2s(st + C::TILE, a.AD + s_ * blk, blk * 8, &full[sl]);
+        bulk_g2s(st + C::TILE + blk, a.Tb + (j > 0 ? s_ - 1 : s_) * blk, blk * 8, &full[sl]);
+        bulk_g2s(st + C::TILE + 2 * blk, a.Dinv + s_ * blk, blk * 8, &full[sl]);
+      }
     }
-  };
-
-  double ser[TM][TN][2];
+    return;
+  }
+  // ---- consumers: warp owns columns [cw, cw+16) of the CTA tile
+  const int cw = warp * 16;
   const bool vec = (K % 2) == 0;
+  double ser[TM][TN][2];
   if (lo < a.n)
     load_tile(ser, a.F + lo * rowK, K, 0, c0 + cw, a.m, g, t, vec);
   else
     zero_acc(ser);
-  if (warp == 0)
-    for (int j = 0; j < NSTG && j < nint; ++j) produce(j);
   double acc[TM][TN][2];
   for (int j = 0; j < nint; ++j) {
-    const int64_t gr = lo + 1 + j;
-    const double* st = stg + (j % NSTG) * C::FWD_STAGE;
-    mbar_wait(&full[j % NSTG], (unsigned)((j / NSTG) & 1));
+    const int sl = j % NSTG;
+    const double* st = stg + sl * C::FWD_STAGE;
+    mbar_wait(&full[sl], (unsigned)((j / NSTG) & 1));
     zero_acc(acc);
     smem_mma<MP, TM, TN>(acc, st + C::TILE + 2 * blk, st, LDT, cw, g, t);  // Dinv_j f_g
     smem_mma<MP, TM, TN>(acc, st + C::TILE, Ys, LDT, cw, g, t);            // AD_j y_{j-1}
     smem_mma<MP, TM, TN>(ser, st + C::TILE + blk, Ys, LDT, cw, g, t);      // Tb_{j-1} y_{j-1}
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[sl]);
     store_smem(acc, Ys, LDT, 0, cw, g, t);
-    store_tile(acc, a.X + gr * rowK, K, 0, c0 + cw, a.m, g, t, vec);
-    __syncthreads();
-    if (warp == 0 && j + NSTG < nint) produce(j + NSTG);
+    store_tile(acc, a.X + (lo + 1 + j) * rowK, K, 0, c0 + cw, a.m, g, t, vec);
+    __syncwarp();
   }
   if (nint > 0) wgemm<MP, TM, TN, 2>(ser, a.Tb + (slot0 + nint - 1) * blk, Ys + cw, LDT, g, t);
   store_tile(ser, a.base + (int64_t)q * a.base_stride, K, 0, c0 + cw, MP, g, t, vec);
 }
 
 template <int MP, int NW, int NSTG>
-__global__ void __launch_bounds__(32 * NW) stream_bwd_kernel(ChainArgs a) {
+__global__ void __launch_bounds__(32 * (NW + 1)) stream_bwd_kernel(ChainArgs a) {
   using C = StreamCfg<MP, NW, NSTG>;
   constexpr int TM = C::TM, TN = C::TN, LDT = C::LDT;
   extern __shared__ __align__(16) double sm[];
@@ -666,17 +676,20 @@ __global__ void __launch_bounds__(32 * NW) stream_bwd_kernel(ChainArgs a) {
   double* Xn = sm + C::TILE;
   double* stg = sm + 2 * C::TILE;
   uint64_t* full = reinterpret_cast<uint64_t*>(stg + NSTG * C::BWD_STAGE);
+  uint64_t* empty = full + NSTG;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int q = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * C::KC;
   const int64_t K = a.K;
   const int ncols = (int)(K - c0 < C::KC ? K - c0 : C::KC);
-  const int cw = warp * 16;
   const bool vec = (K % 2) == 0;
   for (int e = tid; e < 2 * C::TILE + NSTG * C::BWD_STAGE; e += C::NT) sm[e] = 0.0;
   if (tid == 0) {
-    for (int i = 0; i < NSTG; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < NSTG; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NW);
+    }
     mbar_fence_init();
   }
   __syncthreads();
@@ -686,50 +699,51 @@ __global__ void __launch_bounds__(32 * NW) stream_bwd_kernel(ChainArgs a) {
   const int64_t rowK = (int64_t)a.m * K;
   const int64_t xtK = (int64_t)MP * K;
   constexpr int64_t blk = C::BLK;
-
   // x~_q, x~_{q+1} tiles (MP rows of the [nr+1][MP][K] buffer)
   for (int e = tid; e < MP * ncols; e += C::NT) {
     const int r = e / ncols, c = e % ncols;
     Xq[r * LDT + c] = a.xt[(int64_t)q * xtK + (int64_t)r * K + c0 + c];
     Xn[r * LDT + c] = a.xt[(int64_t)(q + 1) * xtK + (int64_t)r * K + c0 + c];
   }
-  if (lo < a.n) {
+  __syncthreads();
+  if (warp == NW) {  // ---- producer: step jj handles row j = nint-1-jj
+    for (int jj = 0; jj < nint; ++jj) {
+      const int j = nint - 1 - jj;
+      const int sl = jj % NSTG;
+      if (jj >= NSTG) mbar_wait(&empty[sl], (unsigned)(((jj / NSTG) - 1) & 1));
+      double* st = stg + sl * C::BWD_STAGE;
+      fence_proxy_async();
+      if (lane == 0) mbar_expect_tx(&full[sl], (unsigned)(a.m * ncols * 8) + 2u * blk * 8u);
+      __syncwarp();
+      issue_tile(st, LDT, a.X + (lo + 1 + j) * rowK + c0, K, a.m, ncols, &full[sl], lane);
+      if (lane == 0) {
+        const int64_t s_ = slot0 + j;
+        bulk_g2s(st + C::TILE, a.G + s_ * blk, blk * 8, &full[sl]);
+        bulk_g2s(st + C::TILE + blk, a.S + s_ * blk, blk * 8, &full[sl]);
+      }
+    }
+    return;
+  }
+  const int cw = warp * 16;
+  if (lo < a.n) {  // x[lo] = x~_q  (ref dichotomy.py:351)
     double xq[TM][TN][2];
     load_tile(xq, a.xt + (int64_t)q * xtK, K, 0, c0 + cw, MP, g, t, vec);
     store_tile(xq, a.X + lo * rowK, K, 0, c0 + cw, a.m, g, t, vec);
   }
-  // step jj handles row j = nint-1-jj
-  auto produce = [&](int jj) {
-    const int j = nint - 1 - jj;
-    double* st = stg + (jj % NSTG) * C::BWD_STAGE;
-    uint64_t* bar = &full[jj % NSTG];
-    fence_proxy_async();
-    if (lane == 0) mbar_expect_tx(bar, (unsigned)(a.m * ncols * 8) + 2u * blk * 8u);
-    __syncwarp();
-    issue_tile(st, LDT, a.X + (lo + 1 + j) * rowK + c0, K, a.m, ncols, bar, lane);
-    if (lane == 0) {
-      const int64_t sl = slot0 + j;
-      bulk_g2s(st + C::TILE, a.G + sl * blk, blk * 8, bar);
-      bulk_g2s(st + C::TILE + blk, a.S + sl * blk, blk * 8, bar);
-    }
-  };
-  __syncthreads();
-  if (warp == 0)
-    for (int jj = 0; jj < NSTG && jj < nint; ++jj) produce(jj);
   for (int jj = 0; jj < nint; ++jj) {
     const int j = nint - 1 - jj;
-    const int64_t gr = lo + 1 + j;
-    const double* st = stg + (jj % NSTG) * C::BWD_STAGE;
-    mbar_wait(&full[jj % NSTG], (unsigned)((jj / NSTG) & 1));
+    const int sl = jj % NSTG;
+    const double* st = stg + sl * C::BWD_STAGE;
+    mbar_wait(&full[sl], (unsigned)((jj / NSTG) & 1));
     double acc[TM][TN][2];
     load_smem(acc, st, LDT, 0, cw, g, t);                                 // y_j
     smem_mma<MP, TM, TN>(acc, st + C::TILE, Xq, LDT, cw, g, t);        // + G_j x~_q
     smem_mma<MP, TM, TN>(acc, st + C::TILE + blk, Xn, LDT, cw, g, t);  // + S_j x_{j+1}
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[sl]);
     store_smem(acc, Xn, LDT, 0, cw, g, t);
-    store_tile(acc, a.X + gr * rowK, K, 0, c0 + cw, a.m, g, t, vec);
-    __syncthreads();
-    if (warp == 0 && jj + NSTG < nint) produce(jj + NSTG);
+    store_tile(acc, a.X + (lo + 1 + j) * rowK, K, 0, c0 + cw, a.m, g, t, vec);
+    __syncwarp();
   }
 }
 

@@ -69,6 +69,9 @@ BTD_DEVINL void mbar_wait(uint64_t* bar, unsigned parity) {
       "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
       "r"(parity));
 }
+BTD_DEVINL void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 // global -> shared bulk copy, completion counted on `bar` (bytes % 16 == 0, 16B-aligned)
 BTD_DEVINL void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
