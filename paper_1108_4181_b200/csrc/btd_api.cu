@@ -40,6 +40,7 @@
 #include "btd_chain.cuh"
 #include "btd_gemm.cuh"
 #include "btd_inv.cuh"
+#include "btd_tree.cuh"
 
 using namespace btd;
 
@@ -361,6 +362,11 @@ struct btd_plan {
   };
   int64_t partial_elems_per_k = 0;  // split-K scratch: doubles per unit K
   DevBuf partial;
+  // fused cooperative tree (M <= 32, single rank)
+  bool fused_tree = false;
+  TreeArgs targs{};
+  int tree_chunks = 0;
+  DevBuf tpartial;
   std::vector<Level> levels;
   // interface-RHS carry (local ranges whose last interior row exists)
   int ncarry = 0;
@@ -1216,6 +1222,43 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
     // split-K plans: enough CTAs (>= 2 waves) for the series sums and the level corrections
     pl.z_k = zrl;
     build_splits(pl);
+    // fused cooperative tree for small blocks on a single rank
+    const char* ft_env = getenv("BTD_FUSED_TREE");
+    if (pl.mode == 0 && mp <= 32 && pl.world == 1 && (!ft_env || atoi(ft_env))) {
+      constexpr int CH = 16;
+      std::vector<int32_t> chn, chb, chc, zco(nn, 0), zcc(nn, 0), he(nn, 0), hh(nn, 0), lvo, lvn;
+      std::vector<int64_t> klist(nn), xlv(nn), xhv(nn);
+      for (int b = 0; b < nn; ++b) {
+        const Node& nd = pl.nodes[b];
+        klist[b] = nd.k;
+        xlv[b] = nd.lo >= 1 ? nd.lo - 1 : nr;
+        xhv[b] = nd.hi + 1 <= nr - 1 ? nd.hi + 1 : nr;
+        he[b] = nd.lo >= 1;
+        hh[b] = nd.hi + 1 <= nr - 1;
+        if (!need_k[nd.k]) continue;
+        zco[b] = (int32_t)chn.size();
+        for (int64_t b0 = 0; b0 < sz[b]; b0 += CH) {
+          chn.push_back(b); chb.push_back((int32_t)b0); chc.push_back((int32_t)std::min<int64_t>(CH, sz[b] - b0));
+        }
+        zcc[b] = (int32_t)chn.size() - zco[b];
+      }
+      for (int64_t lev = 0; lev <= maxlevel; ++lev) {
+        lvo.push_back((int32_t)lvn.size());
+        for (int b = 0; b < nn; ++b)
+          if (pl.nodes[b].level == lev && need_k[pl.nodes[b].k]) lvn.push_back(b);
+      }
+      lvo.push_back((int32_t)lvn.size());
+      TreeArgs& ta = pl.targs;
+      ta.nchunks = (int)chn.size();
+      ta.nlev = (int)maxlevel + 1;
+      ta.ch_node = pl.upload(chn); ta.ch_blk0 = pl.upload(chb); ta.ch_nblk = pl.upload(chc);
+      ta.roff = pl.upload(roff); ta.rld = pl.upload(rld); ta.lo = pl.d_nlo ? pl.d_nlo : nullptr;
+      ta.k = pl.upload(klist); ta.zc_off = pl.upload(zco); ta.zc_cnt = pl.upload(zcc);
+      ta.xl = pl.upload(xlv); ta.xh = pl.upload(xhv); ta.has_e = pl.upload(he); ta.has_h = pl.upload(hh);
+      ta.lv_off = pl.upload(lvo); ta.lv_nodes = pl.upload(lvn);
+      pl.tree_chunks = ta.nchunks;
+      pl.fused_tree = true;
+    }
   }
   CK(cudaStreamSynchronize(st));
   pl.factor_bytes += (int64_t)(rtot + 2 * nn * blk) * sizeof(double);
@@ -1234,6 +1277,7 @@ void ensure_scratch(btd_plan& pl, int64_t K) {
   pl.xt.alloc((size_t)(pl.nr + 1) * mpK * sizeof(double));
   CK(cudaMemset(pl.xt.p, 0, (size_t)(pl.nr + 1) * mpK * sizeof(double)));
   CK(cudaMemset(pl.ft.p, 0, (size_t)pl.nr * mpK * sizeof(double)));
+  if (pl.fused_tree) pl.tpartial.alloc((size_t)std::max(pl.tree_chunks, 1) * pl.mp * K * sizeof(double));
   if (pl.partial_elems_per_k) {
     pl.partial.alloc((size_t)pl.partial_elems_per_k * K * sizeof(double));
     pl.z_split.partial = pl.partial.d();
@@ -1304,9 +1348,41 @@ void solve_levels(btd_plan& pl, int64_t K, cudaStream_t st) {
                 st, &lev.split);
 }
 
+template <int MP>
+void launch_tree_small(btd_plan& pl, int64_t K, cudaStream_t st) {
+  static int max_blocks = -1, nsm = 0;
+  if (max_blocks < 0) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks, tree_small_kernel<MP>, 256, 0));
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  TreeArgs ta = pl.targs;
+  ta.K = K;
+  ta.R = pl.Rrows.d();
+  ta.EH = pl.EH.d();
+  ta.ft = pl.ft.d();
+  ta.partial = pl.tpartial.d();
+  ta.xt = pl.xt.d();
+  const int ntile = (int)((K + 15) / 16);
+  const int64_t work = (int64_t)std::max(ta.nchunks, 1) * ntile;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)max_blocks * nsm, (work + 7) / 8));
+  void* args[] = {&ta};
+  CK(cudaLaunchCooperativeKernel((const void*)tree_small_kernel<MP>, dim3(grid), dim3(256), args, 0, st));
+  CK_LAUNCH();
+}
+
 // Algorithm 1 on the interface system: z = R f~ (all needed nodes), then the levels.
 void solve_tree(btd_plan& pl, int64_t K, cudaStream_t st) {
   const int64_t mp = pl.mp, mpK = mp * K;
+  if (pl.fused_tree) {
+    switch (mp) {
+      case 8: launch_tree_small<8>(pl, K, st); return;
+      case 16: launch_tree_small<16>(pl, K, st); return;
+      case 32: launch_tree_small<32>(pl, K, st); return;
+      default: break;
+    }
+  }
   launch_gemm(mp, K, pl.nz, mk(pl.zbuf.d(), pl.z_id, 0, mpK, K), none(), 0.0,
               {term(mk(pl.Rrows.d(), pl.z_roff, 0, 1, 0, pl.z_rld), mk(pl.ft.d(), pl.z_nlo, 0, mpK, K), 0, 1.0,
                     pl.z_rld)},

@@ -1,0 +1,158 @@
+// Fused Algorithm 1 (reduced interface solve) for small blocks, one cooperative launch.
+//
+// Reference: dichotomy.py:279-295 (reduced_solve) -- per tree node, in BFS order,
+// x~_k = R_node f~[lo..hi] with the end corrections applied from the parent
+// splits.  Written as   x~_k = z_node + E_node x~_{lo-1} + H_node x~_{hi+1},
+// z_node = R_node f~[lo..hi]  (E, H precomputed at plan time).
+//
+// For M <= 32 the GEMM-per-level formulation is launch-latency-bound (a c4 plan has
+// 592 ranges and 11 tree levels: ~25 dependent launches of tiny GEMMs).  Here:
+//   phase 1: the series sums are cut into chunks of CH blocks; every (chunk,
+//            16-column tile) item is one warp-level DMMA product (all independent);
+//   grid sync;
+//   phase 2: level by level, x~_k = sum of the node's chunk partials (fixed order,
+//            deterministic) + E x~ + H x~, one grid sync per level.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "btd_common.cuh"
+
+namespace btd {
+
+struct TreeArgs {
+  int nchunks, nlev;
+  int64_t K;
+  // chunks
+  const int32_t* ch_node;
+  const int32_t* ch_blk0;
+  const int32_t* ch_nblk;
+  // per node
+  const int64_t* roff;
+  const int64_t* rld;
+  const int64_t* lo;
+  const int64_t* k;
+  const int32_t* zc_off;
+  const int32_t* zc_cnt;
+  const int64_t* xl;
+  const int64_t* xh;
+  const int32_t* has_e;
+  const int32_t* has_h;
+  // levels: nodes of level l are lv_nodes[lv_off[l] .. lv_off[l+1])
+  const int32_t* lv_off;
+  const int32_t* lv_nodes;
+  const double* R;    // inverse rows
+  const double* EH;   // [2*nodes][MP][MP]
+  const double* ft;   // [nr][MP][K]
+  double* partial;    // [nchunks][MP][K]
+  double* xt;         // [nr+1][MP][K]
+};
+
+// acc(MP x 16) += A(MP x MP, global, row stride lda) @ B(MP x 16 cols from col0, global, row stride ldb)
+template <int MP, int TM, int TN>
+BTD_DEVINL void gmem_mma(double (&acc)[TM][TN][2], const double* __restrict__ A, int64_t lda,
+                         const double* __restrict__ B, int64_t ldb, int64_t col0, int64_t K, int g, int t) {
+#pragma unroll
+  for (int s = 0; s < MP / 8; ++s) {
+    double2 a[TM];
+    double b0[TN], b1[TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) a[i] = ldg_cg2(A + (int64_t)(i * 8 + g) * lda + 8 * s + 2 * t);
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t c = col0 + j * 8 + g;
+      b0[j] = c < K ? __ldcg(B + (int64_t)(8 * s + 2 * t) * ldb + j * 8 + g) : 0.0;
+      b1[j] = c < K ? __ldcg(B + (int64_t)(8 * s + 2 * t + 1) * ldb + j * 8 + g) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b0[j]);
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b1[j]);
+  }
+}
+
+template <int TM, int TN>
+BTD_DEVINL void acc_add_tile(double (&acc)[TM][TN][2], const double* __restrict__ P, int64_t K, int64_t col0, int g,
+                             int t) {
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t c = col0 + j * 8 + 2 * t;
+      const double* p = P + (int64_t)(i * 8 + g) * K + c;
+      if (c < K) acc[i][j][0] += __ldcg(p);
+      if (c + 1 < K) acc[i][j][1] += __ldcg(p + 1);
+    }
+}
+
+template <int TM, int TN>
+BTD_DEVINL void acc_store_tile(const double (&acc)[TM][TN][2], double* __restrict__ P, int64_t K, int64_t col0,
+                               int g, int t) {
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t c = col0 + j * 8 + 2 * t;
+      double* p = P + (int64_t)(i * 8 + g) * K + c;
+      if (c < K) __stcg(p, acc[i][j][0]);
+      if (c + 1 < K) __stcg(p + 1, acc[i][j][1]);
+    }
+}
+
+template <int MP>
+__global__ void __launch_bounds__(256) tree_small_kernel(TreeArgs a) {
+  namespace cg = cooperative_groups;
+  constexpr int TM = MP / 8, TN = 2;
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  const int64_t K = a.K, mpK = (int64_t)MP * K;
+  const int ntile = (int)((K + 15) / 16);
+  constexpr int64_t blk = (int64_t)MP * MP;
+
+  // phase 1: chunk partial series sums  partial[c] = sum_blk R_b[:, blk] f~[lo_b + blk]
+  for (int item = gw; item < a.nchunks * ntile; item += nw) {
+    const int c = item / ntile;
+    const int64_t col0 = (int64_t)(item % ntile) * 16;
+    const int b = a.ch_node[c];
+    double acc[TM][TN][2];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int64_t ld = a.rld[b];
+    for (int e = 0; e < a.ch_nblk[c]; ++e) {
+      const int64_t bk = a.ch_blk0[c] + e;
+      gmem_mma<MP, TM, TN>(acc, a.R + a.roff[b] + bk * MP, ld, a.ft + (a.lo[b] + bk) * mpK + col0, K, col0, K, g, t);
+    }
+    acc_store_tile(acc, a.partial + (int64_t)c * mpK, K, col0, g, t);
+  }
+  grid.sync();
+  // phase 2: levels
+  for (int l = 0; l < a.nlev; ++l) {
+    const int n0 = a.lv_off[l], n1 = a.lv_off[l + 1];
+    for (int item = gw; item < (n1 - n0) * ntile; item += nw) {
+      const int b = a.lv_nodes[n0 + item / ntile];
+      const int64_t col0 = (int64_t)(item % ntile) * 16;
+      double acc[TM][TN][2];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int c = 0; c < a.zc_cnt[b]; ++c) acc_add_tile(acc, a.partial + (int64_t)(a.zc_off[b] + c) * mpK, K, col0, g, t);
+      if (a.has_e[b])
+        gmem_mma<MP, TM, TN>(acc, a.EH + (2 * (int64_t)b) * blk, MP, a.xt + a.xl[b] * mpK + col0, K, col0, K, g, t);
+      if (a.has_h[b])
+        gmem_mma<MP, TM, TN>(acc, a.EH + (2 * (int64_t)b + 1) * blk, MP, a.xt + a.xh[b] * mpK + col0, K, col0, K, g,
+                             t);
+      acc_store_tile(acc, a.xt + a.k[b] * mpK, K, col0, g, t);
+    }
+    grid.sync();
+  }
+}
+
+}  // namespace btd
