@@ -480,12 +480,58 @@ def residual_check(torch, name, X, F, configs):
     return r
 
 
+def run_dd(args):
+    """--config c3dd: the full Schur-complement DD solve of config 3's grid
+    (SURVEY.md 8f row f1): interiors by stacked dichotomy plans, interface by the
+    S-plan, recovery -- RHS/s of whole-grid solves."""
+    import torch
+
+    from paper_1108_4181_b200 import _native, configs, schur
+
+    cfg = configs.CONFIGS["c3"]
+    nx, nz, nsub, K = cfg["nx"], cfg["nz"], cfg["nsub"], cfg["k"]
+    torch.cuda.set_device(0)
+    t0 = time.perf_counter()
+    dd = schur.HelmholtzDD(nx, nz, nsub, groups=4)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    g = torch.Generator(device="cuda")
+    g.manual_seed(0)
+    f = torch.randn((nz, nx, K), dtype=torch.float64, device="cuda", generator=g)
+    for _ in range(args.warmup):
+        x = dd.solve(f)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lc0 = _native.launch_count()
+    with ClockSampler(0) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            x = dd.solve(f)
+        e1.record()
+        e1.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    res = dd.residual(x, f)
+    fp64 = fp64_peak_tflops(torch)
+    ni = [e - a for a, e in dd.sub]
+    flops = 2 * sum(10.0 * nx * n * n * K for n in ni) + 10.0 * (nsub - 1) * nx * nx * K
+    line = {"metric": "rhs_columns_per_second", "value": K / (ms / 1e3), "unit": "RHS/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "none", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded layered velocity model, torch Philox RHS)",
+            "config": {"workload": "c3dd", "nx": nx, "nz": nz, "nsub": nsub, "k": K, "interior_groups": 4},
+            "solve_roofline": {"flops": flops, "t_roof_ms": flops / (fp64 * 1e12) * 1e3,
+                               "frac": flops / (fp64 * 1e12) * 1e3 / ms, "fp64_tflops_peak": fp64},
+            "plan_build_s": build_s, "grid_rel_residual": res, "clocks": clk.summary(),
+            "gpu_launches": _native.launch_count() - lc0}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c1"), choices=sorted(BENCH_CFG))
+    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c1"), choices=sorted(BENCH_CFG) + ["c3dd"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ranks", type=int, default=0)
     ap.add_argument("--split", type=int, default=0)
@@ -496,6 +542,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c3dd":
+        run_dd(args)
     else:
         run_b200(args)
 

@@ -164,3 +164,122 @@ def interface_rhs_from_grid(fgrid, nx, nz, nsub, **kw):
         if i < nsub - 1:
             out[i] += w[-1]
     return out
+
+
+class HelmholtzDD:
+    """Full Schur-complement DD solve of the config-3 operator on the GPU
+    (ref schur.py:322-372 solve_schur = schur_rhs ->
+    solve_interface -> recover_interiors).
+
+    * Interiors: subdomain i (z rows a_i..b_i-1) in the reference's
+      block-per-x-column orientation (acoustic.py:231-243): nx block rows of
+      order n_i <= Mi with C = tridiag(-1, 4 + s_z, -1) over z and A = B = I.
+      ``groups`` plans each stack nsub/groups subdomains (zero couplings between
+      them, blocks identity-padded to Mi) -- every A_ii^{-1} of a group is ONE
+      dichotomy solve.
+    * Interface: the explicit S (schur_blocks_torch) solved by its own plan.
+    * solve(f): f (nz, nx, K) on the device -> x (nz, nx, K).
+    """
+
+    def __init__(self, nx, nz, nsub, *, h=5.0, sigma=50.0, layers=16, seed=0, groups=1, ranks_int=None,
+                 split_int=1, ranks_s=None, device="cuda"):
+        import torch
+
+        from .dichotomy import plan_build_arrays
+
+        self.torch = torch
+        self.nx, self.nz, self.nsub, self.groups = nx, nz, nsub, groups
+        if nsub % groups:
+            raise ValueError("nsub must be a multiple of groups")
+        self.device = device
+        self.sh = torch.from_numpy(shifts(nz, h, sigma, layers, seed)).to(device)
+        self.z_if = interface_rows(nz, nsub)
+        b = np.concatenate([[-1], self.z_if, [nz]])
+        self.sub = [(int(b[i] + 1), int(b[i + 1])) for i in range(nsub)]
+        self.Mi = max(e - a for a, e in self.sub)
+        Mi = self.Mi
+        per = nsub // groups
+        self.plans = []
+        for gidx in range(groups):
+            subs = self.sub[gidx * per:(gidx + 1) * per]
+            n = per * nx
+            diag = torch.zeros((per, Mi, Mi), dtype=torch.float64, device=device)
+            eye = torch.zeros((per, Mi, Mi), dtype=torch.float64, device=device)
+            for j, (a, e) in enumerate(subs):
+                ni = e - a
+                d = torch.diag(4.0 + self.sh[a:e]) - torch.diag(torch.ones(ni - 1, dtype=torch.float64,
+                                                                             device=device), 1) \
+                    - torch.diag(torch.ones(ni - 1, dtype=torch.float64, device=device), -1)
+                diag[j, :ni, :ni] = d
+                diag[j, ni:, ni:] = torch.eye(Mi - ni, dtype=torch.float64, device=device)
+                eye[j, :ni, :ni] = torch.eye(ni, dtype=torch.float64, device=device)
+            D = diag.repeat_interleave(nx, dim=0).contiguous()
+            cpl = eye.repeat_interleave(nx, dim=0)[: n - 1].clone()
+            cpl[nx - 1::nx] = 0.0  # no coupling across subdomain boundaries
+            P = ranks_int or max(1, min(n, 9 * per))
+            self.plans.append(plan_build_arrays(D, cpl, cpl, P, split=split_int, device=device))
+            del D, cpl
+        d, lo, up = schur_blocks_torch(nx, nz, nsub, device=device, h=h, sigma=sigma, layers=layers, seed=seed)
+        self.plan_s = plan_build_arrays(d, lo, up, ranks_s or min(9, nsub - 1), device=device)
+        del d, lo, up
+        torch.cuda.empty_cache()
+
+    def _stack(self, f, gidx):
+        """grid rows of the group's subdomains -> (per*nx, Mi, K) interior blocks."""
+        torch = self.torch
+        per = self.nsub // self.groups
+        K = f.shape[2]
+        out = torch.zeros((per * self.nx, self.Mi, K), dtype=torch.float64, device=f.device)
+        for j, (a, e) in enumerate(self.sub[gidx * per:(gidx + 1) * per]):
+            out[j * self.nx:(j + 1) * self.nx, : e - a] = f[a:e].permute(1, 0, 2)
+        return out
+
+    def solve(self, f):
+        """x = A^{-1} f by Schur-complement DD (f, x: (nz, nx, K) CUDA tensors)."""
+        from .dichotomy import plan_solve
+
+        torch = self.torch
+        nx, per = self.nx, self.nsub // self.groups
+        K = f.shape[2]
+        # 1. interior solves g_i = A_ii^{-1} f_i   (ref schur.py:322-328)
+        fg = f[torch.as_tensor(self.z_if, device=f.device)].clone()  # (N, nx, K) interface RHS
+        stacked = [self._stack(f, gidx) for gidx in range(self.groups)]
+        for gidx in range(self.groups):
+            g = plan_solve(self.plans[gidx], stacked[gidx])
+            for j in range(per):
+                i = gidx * per + j
+                a, e = self.sub[i]
+                gi = g[j * nx:(j + 1) * nx]  # (nx, Mi, K)
+                if i >= 1:              # interface above: -A_G,i A_ii^{-1} f_i = + first row
+                    fg[i - 1] += gi[:, 0]
+                if i < self.nsub - 1:   # interface below: + last interior row
+                    fg[i] += gi[:, e - a - 1]
+            del g
+        # 2. interface solve S x_G = f~_G (the dichotomy S-solve)
+        xg = plan_solve(self.plan_s, fg.contiguous())
+        # 3. recovery x_i = A_ii^{-1} (f_i - A_iG x_G)   (ref schur.py:331-335)
+        x = torch.empty_like(f)
+        x[torch.as_tensor(self.z_if, device=f.device)] = xg
+        for gidx in range(self.groups):
+            h_ = stacked[gidx]
+            for j in range(per):
+                i = gidx * per + j
+                a, e = self.sub[i]
+                if i >= 1:
+                    h_[j * nx:(j + 1) * nx, 0] += xg[i - 1]
+                if i < self.nsub - 1:
+                    h_[j * nx:(j + 1) * nx, e - a - 1] += xg[i]
+            xi = plan_solve(self.plans[gidx], h_)
+            for j in range(per):
+                a, e = self.sub[gidx * per + j]
+                x[a:e] = xi[j * nx:(j + 1) * nx, : e - a].permute(1, 0, 2)
+        return x
+
+    def residual(self, x, f):
+        """max|A x - f| / max|f| on the grid (5-point operator)."""
+        r = (4.0 + self.sh)[:, None, None] * x - f
+        r[1:] -= x[:-1]
+        r[:-1] -= x[1:]
+        r[:, 1:] -= x[:, :-1]
+        r[:, :-1] -= x[:, 1:]
+        return float(r.abs().max() / f.abs().max())
