@@ -193,6 +193,20 @@ __global__ void lu_pivot_check_kernel(const double* D, const double* LU, int m, 
   }
 }
 
+// cudaFuncSetAttribute is per device: remember which (kernel, device) pairs were set.
+void set_smem_attr(const void* fn, size_t smem) {
+  if (smem <= 48 * 1024) return;
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& d : done)
+    if (d.first == fn && d.second == dev) return;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  done.push_back({fn, dev});
+}
+
 Opnd mk(const double* base, const int64_t* idx, int64_t add, int64_t stride, int64_t ld,
         const int64_t* ld_arr = nullptr) {
   Opnd o;
@@ -244,41 +258,15 @@ void launch_gemm(int64_t rows, int64_t cols, int nbatch, Opnd C, Opnd Cin, doubl
   d.nterms = 0;
   for (const Term& t : terms) d.t[d.nterms++] = t;
   const int gz = std::min(d.split_b ? d.nsplit_total : nbatch, 65535);
-  static int legacy = -1;
-  if (legacy < 0) {
-    const char* e = getenv("BTD_GEMM_LEGACY");
-    legacy = e ? atoi(e) : 0;
-  }
-  if (legacy && !d.split_b) {
-    if (rows <= 32 || cols <= 32) {
-      dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32), gz);
-      gemm_batched_kernel<32, 32><<<grid, 128, 0, st>>>(d);
-    } else {
-      dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64), gz);
-      gemm_batched_kernel<64, 64><<<grid, 128, 0, st>>>(d);
-    }
-    CK_LAUNCH();
-    return;
-  }
   auto tiles = [&](int64_t bm, int64_t bn) { return ((rows + bm - 1) / bm) * ((cols + bn - 1) / bn) * gz; };
   if (rows >= 128 && cols >= 64 && tiles(128, 64) >= 148) {
     using C_ = PipeCfg<128, 64, 4, 2, 3>;
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(gemm_pipe_kernel<128, 64, 4, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)C_::SMEM));
-      attr = true;
-    }
+    set_smem_attr((const void*)gemm_pipe_kernel<128, 64, 4, 2, 3>, C_::SMEM);
     dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 127) / 128), gz);
     gemm_pipe_kernel<128, 64, 4, 2, 3><<<grid, C_::NT, C_::SMEM, st>>>(d);
   } else if (rows > 32 && cols > 32) {
     using C_ = PipeCfg<64, 64, 2, 2, 4>;
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(gemm_pipe_kernel<64, 64, 2, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)C_::SMEM));
-      attr = true;
-    }
+    set_smem_attr((const void*)gemm_pipe_kernel<64, 64, 2, 2, 4>, C_::SMEM);
     dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64), gz);
     gemm_pipe_kernel<64, 64, 2, 2, 4><<<grid, C_::NT, C_::SMEM, st>>>(d);
   } else {
@@ -563,8 +551,7 @@ void launch_inv(btd_plan& pl, int nbatch, const double* in, const int64_t* idx_i
   d.ws = ws.d();
   const int nt = mp <= 16 ? 128 : (mp <= 64 ? 256 : 512);
   const size_t smem = use_smem ? wbytes : 0;
-  if (use_smem && smem > 48 * 1024)
-    CK(cudaFuncSetAttribute(gj_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (use_smem) set_smem_attr((const void*)gj_inverse_kernel, smem);
   gj_inverse_kernel<<<grid, nt, smem, st>>>(d, use_smem);
   CK_LAUNCH();
 }
@@ -577,14 +564,10 @@ void launch_chain_t(const ChainArgs& a, bool fwd, cudaStream_t st) {
   const int64_t ntile = (a.K + KT - 1) / KT;
   dim3 grid((unsigned)ntile, (unsigned)a.nr);
   if (fwd) {
-    if (smem > 48 * 1024)
-      CK(cudaFuncSetAttribute(chain_fwd_kernel<MP, KT, WR, WC, NF, NY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)smem));
+    set_smem_attr((const void*)chain_fwd_kernel<MP, KT, WR, WC, NF, NY>, smem);
     chain_fwd_kernel<MP, KT, WR, WC, NF, NY><<<grid, Cfg::NT, smem, st>>>(a);
   } else {
-    if (smem > 48 * 1024)
-      CK(cudaFuncSetAttribute(chain_bwd_kernel<MP, KT, WR, WC, NF, NY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)smem));
+    set_smem_attr((const void*)chain_bwd_kernel<MP, KT, WR, WC, NF, NY>, smem);
     chain_bwd_kernel<MP, KT, WR, WC, NF, NY><<<grid, Cfg::NT, smem, st>>>(a);
   }
   CK_LAUNCH();
@@ -596,10 +579,10 @@ void launch_stream_t(const ChainArgs& a, bool fwd, cudaStream_t st) {
   const size_t smem = fwd ? C::FWD_SMEM : C::BWD_SMEM;
   dim3 grid((unsigned)((a.K + C::KC - 1) / C::KC), (unsigned)a.nr);
   if (fwd) {
-    CK(cudaFuncSetAttribute(stream_fwd_kernel<MP, NW, NSTG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_smem_attr((const void*)stream_fwd_kernel<MP, NW, NSTG>, smem);
     stream_fwd_kernel<MP, NW, NSTG><<<grid, C::NT, smem, st>>>(a);
   } else {
-    CK(cudaFuncSetAttribute(stream_bwd_kernel<MP, NW, NSTG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_smem_attr((const void*)stream_bwd_kernel<MP, NW, NSTG>, smem);
     stream_bwd_kernel<MP, NW, NSTG><<<grid, C::NT, smem, st>>>(a);
   }
   CK_LAUNCH();
@@ -659,18 +642,6 @@ int64_t pad_order(int64_t m, int mode) {
   for (int64_t c : {8, 16, 32, 64, 128, 256})
     if (m <= c) return c;
   return (m + 7) / 8 * 8;
-}
-
-// f~_q = base_q + carry_{q-1}  from the all-gathered (base, carry) pairs
-__global__ void assemble_ft_kernel(const double* exch, double* ft, int64_t nr, int64_t mpK) {
-  const int64_t total = nr * mpK;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t q = e / mpK, r = e % mpK;
-    double v = exch[(2 * q) * mpK + r];
-    if (q >= 1) v += exch[(2 * (q - 1) + 1) * mpK + r];
-    ft[e] = v;
-  }
 }
 
 // ---------------------------------------------------------------- plan build, local part
@@ -1350,13 +1321,10 @@ void solve_levels(btd_plan& pl, int64_t K, cudaStream_t st) {
 
 template <int MP>
 void launch_tree_small(btd_plan& pl, int64_t K, cudaStream_t st) {
-  static int max_blocks = -1, nsm = 0;
-  if (max_blocks < 0) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks, tree_small_kernel<MP>, 256, 0));
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  }
+  int max_blocks = 0, nsm = 0, dev = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks, tree_small_kernel<MP>, 256, 0));
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   TreeArgs ta = pl.targs;
   ta.K = K;
   ta.R = pl.Rrows.d();
