@@ -377,8 +377,19 @@ struct btd_plan {
   std::vector<Step1> steps1;
   int nlive = 0;  // local ranges whose interface row is < n
   // scratch
-  int64_t scratch_k = 0;
-  DevBuf ft, zbuf, xt, hostio, fcopy;  // fcopy: mode-1 staging of F when it aliases X
+  // per-solve scratch; two slots so the pipelined host path can run two column
+  // chunks concurrently on two streams (fcopy: mode-1 staging of F aliasing X)
+  struct Scratch {
+    int64_t k = 0;
+    DevBuf ft, zbuf, xt, partial, tpartial, fcopy;
+    cudaStream_t own = nullptr;  // graph replay stream
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  };
+  static constexpr int kSlots = 4;  // host pipeline: chunk c solves in slot c % nstreams
+  Scratch sc[kSlots];
+  int cur = 0;
+  Scratch& S() { return sc[cur]; }
+  DevBuf hostio;
   int64_t hostio_k = 0;
   std::mutex mu;
   cudaStream_t last_stream = nullptr;
@@ -388,18 +399,18 @@ struct btd_plan {
     const double* F;
     double* X;
     int64_t K;
+    int slot;
     int calls;
     cudaGraphExec_t exec;
     int64_t nkern;
   };
   std::vector<GraphEntry> graphs;
-  cudaStream_t own = nullptr;
   // pipelined host path: copy-in / copy-out streams, double-buffered column chunks
-  cudaStream_t s_in = nullptr, s_out = nullptr;
-  cudaEvent_t ev_h[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
-  DevBuf hchunk[2];
+  cudaStream_t s_in = nullptr, s_out = nullptr, s_c[kSlots - 1] = {};  // extra compute streams
+  static constexpr int kHostBufs = 8;  // device chunk buffers of the host pipeline
+  cudaEvent_t ev_h[kHostBufs][3] = {};
+  DevBuf hchunk;  // kHostBufs x chunk elements
   int64_t hchunk_elems = 0;
-  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   // cuSOLVER for block orders above 256 (preprocessing only)
   cusolverDnHandle_t solver = nullptr;
   DevBuf sv_work, sv_ipiv, sv_info, sv_lu;
@@ -438,14 +449,18 @@ struct btd_plan {
     if (solver) cusolverDnDestroy(solver);
     for (auto& g : graphs)
       if (g.exec) cudaGraphExecDestroy(g.exec);
-    if (own) cudaStreamDestroy(own);
+    for (auto& x : sc) {
+      if (x.own) cudaStreamDestroy(x.own);
+      if (x.ev_in) cudaEventDestroy(x.ev_in);
+      if (x.ev_out) cudaEventDestroy(x.ev_out);
+    }
     if (s_in) cudaStreamDestroy(s_in);
     if (s_out) cudaStreamDestroy(s_out);
+    for (auto x : s_c)
+      if (x) cudaStreamDestroy(x);
     for (auto& a : ev_h)
       for (auto& e : a)
         if (e) cudaEventDestroy(e);
-    if (ev_in) cudaEventDestroy(ev_in);
-    if (ev_out) cudaEventDestroy(ev_out);
   }
   template <class T>
   const T* upload(const std::vector<T>& v) {
@@ -1238,23 +1253,21 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
 
 // ---------------------------------------------------------------- solve
 void ensure_scratch(btd_plan& pl, int64_t K) {
-  if (pl.scratch_k == K) return;
+  auto& S = pl.S();
+  if (S.k == K) return;
+  std::vector<btd_plan::GraphEntry> keep;  // graphs of this slot point at the old buffers
   for (auto& g : pl.graphs)
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-  pl.graphs.clear();  // captured graphs point at the old scratch
+    if (g.slot == pl.cur) { if (g.exec) cudaGraphExecDestroy(g.exec); } else keep.push_back(g);
+  pl.graphs.swap(keep);
   const int64_t mpK = pl.mp * K;
-  pl.ft.alloc((size_t)pl.nr * mpK * sizeof(double));
-  pl.zbuf.alloc((size_t)pl.nodes.size() * mpK * sizeof(double));
-  pl.xt.alloc((size_t)(pl.nr + 1) * mpK * sizeof(double));
-  CK(cudaMemset(pl.xt.p, 0, (size_t)(pl.nr + 1) * mpK * sizeof(double)));
-  CK(cudaMemset(pl.ft.p, 0, (size_t)pl.nr * mpK * sizeof(double)));
-  if (pl.fused_tree) pl.tpartial.alloc((size_t)std::max(pl.tree_chunks, 1) * pl.mp * K * sizeof(double));
-  if (pl.partial_elems_per_k) {
-    pl.partial.alloc((size_t)pl.partial_elems_per_k * K * sizeof(double));
-    pl.z_split.partial = pl.partial.d();
-    for (auto& L_ : pl.levels) L_.split.partial = pl.partial.d();
-  }
-  pl.scratch_k = K;
+  S.ft.alloc((size_t)pl.nr * mpK * sizeof(double));
+  S.zbuf.alloc((size_t)pl.nodes.size() * mpK * sizeof(double));
+  S.xt.alloc((size_t)(pl.nr + 1) * mpK * sizeof(double));
+  CK(cudaMemset(S.xt.p, 0, (size_t)(pl.nr + 1) * mpK * sizeof(double)));
+  CK(cudaMemset(S.ft.p, 0, (size_t)pl.nr * mpK * sizeof(double)));
+  if (pl.fused_tree) S.tpartial.alloc((size_t)std::max(pl.tree_chunks, 1) * pl.mp * K * sizeof(double));
+  if (pl.partial_elems_per_k) S.partial.alloc((size_t)pl.partial_elems_per_k * K * sizeof(double));
+  S.k = K;
 }
 
 ChainArgs chain_args(btd_plan& pl, const double* F, double* X, int64_t K, double* base, int64_t base_stride) {
@@ -1266,7 +1279,7 @@ ChainArgs chain_args(btd_plan& pl, const double* F, double* X, int64_t K, double
   a.AD = pool + pl.off_AD * blk; a.Dinv = pool + pl.off_Dinv * blk; a.Tb = pool + pl.off_Tb * blk;
   a.S = pool + pl.off_S * blk; a.G = pool + pl.off_G * blk;
   a.base = base; a.base_stride = base_stride;
-  a.xt = pl.xt.d() + pl.q0 * pl.mp * K;
+  a.xt = pl.S().xt.d() + pl.q0 * pl.mp * K;
   return a;
 }
 
@@ -1285,9 +1298,10 @@ void solve_forward(btd_plan& pl, const double* F, double* X, int64_t K, double* 
   const size_t fbytes = (size_t)pl.nloc * mK * sizeof(double);
   const char *f0 = (const char*)F, *x0 = (const char*)X;
   if (fbytes && f0 < x0 + fbytes && x0 < f0 + fbytes) {
-    if (pl.fcopy.bytes < fbytes) pl.fcopy.alloc(fbytes);
-    CK(cudaMemcpyAsync(pl.fcopy.p, F, fbytes, cudaMemcpyDeviceToDevice, st));
-    F = pl.fcopy.d();
+    auto& fc = pl.S().fcopy;
+    if (fc.bytes < fbytes) fc.alloc(fbytes);
+    CK(cudaMemcpyAsync(fc.p, F, fbytes, cudaMemcpyDeviceToDevice, st));
+    F = fc.d();
   }
   // mode 1: base_q = F[lo_q] (rows < m; pad rows stay 0), then one GEMM launch per row step
   launch_gemm(m, K, pl.nlive, mk(base, nullptr, 0, base_stride, K), mk(F, pl.d_lo, 0, mK, K), 1.0, {}, st);
@@ -1307,16 +1321,24 @@ void solve_forward(btd_plan& pl, const double* F, double* X, int64_t K, double* 
   }
 }
 
+// split-K maps with the current scratch slot's partial buffer
+const SplitK* split_with(const SplitK& sp, btd_plan& pl) {
+  static thread_local SplitK tmp;
+  tmp = sp;
+  tmp.partial = pl.S().partial.d();
+  return &tmp;
+}
+
 // Algorithm 1, level part: x~_k = z_node + E x~_{lo-1} + H x~_{hi+1}, level by level.
 void solve_levels(btd_plan& pl, int64_t K, cudaStream_t st) {
   const int64_t mp = pl.mp, blk = pl.blk, mpK = mp * K;
-  double* xt = pl.xt.d();
-  double* z = pl.zbuf.d();
+  double* xt = pl.S().xt.d();
+  double* z = pl.S().zbuf.d();
   for (const auto& lev : pl.levels)
     launch_gemm(mp, K, lev.count, mk(xt, lev.c_idx, 0, mpK, K), mk(z, lev.z_idx, 0, mpK, K), 1.0,
                 {term(mk(pl.EH.d(), lev.e_idx, 0, blk, mp), mk(xt, lev.xl_idx, 0, mpK, K), mp, 1.0, lev.e_k),
                  term(mk(pl.EH.d(), lev.h_idx, 0, blk, mp), mk(xt, lev.xh_idx, 0, mpK, K), mp, 1.0, lev.h_k)},
-                st, &lev.split);
+                st, split_with(lev.split, pl));
 }
 
 template <int MP>
@@ -1329,9 +1351,9 @@ void launch_tree_small(btd_plan& pl, int64_t K, cudaStream_t st) {
   ta.K = K;
   ta.R = pl.Rrows.d();
   ta.EH = pl.EH.d();
-  ta.ft = pl.ft.d();
-  ta.partial = pl.tpartial.d();
-  ta.xt = pl.xt.d();
+  ta.ft = pl.S().ft.d();
+  ta.partial = pl.S().tpartial.d();
+  ta.xt = pl.S().xt.d();
   const int ntile = (int)((K + 15) / 16);
   const int64_t work = (int64_t)std::max(ta.nchunks, 1) * ntile;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)max_blocks * nsm, (work + 7) / 8));
@@ -1351,10 +1373,10 @@ void solve_tree(btd_plan& pl, int64_t K, cudaStream_t st) {
       default: break;
     }
   }
-  launch_gemm(mp, K, pl.nz, mk(pl.zbuf.d(), pl.z_id, 0, mpK, K), none(), 0.0,
-              {term(mk(pl.Rrows.d(), pl.z_roff, 0, 1, 0, pl.z_rld), mk(pl.ft.d(), pl.z_nlo, 0, mpK, K), 0, 1.0,
+  launch_gemm(mp, K, pl.nz, mk(pl.S().zbuf.d(), pl.z_id, 0, mpK, K), none(), 0.0,
+              {term(mk(pl.Rrows.d(), pl.z_roff, 0, 1, 0, pl.z_rld), mk(pl.S().ft.d(), pl.z_nlo, 0, mpK, K), 0, 1.0,
                     pl.z_rld)},
-              st, &pl.z_split);
+              st, split_with(pl.z_split, pl));
   solve_levels(pl, K, st);
 }
 
@@ -1362,7 +1384,7 @@ void solve_tree(btd_plan& pl, int64_t K, cudaStream_t st) {
 void solve_backward(btd_plan& pl, const double* F, double* X, int64_t K, cudaStream_t st) {
   const int64_t mp = pl.mp, m = pl.m, blk = pl.blk, mpK = mp * K, mK = m * K;
   double* pool = pl.pool.d();
-  double* xt = pl.xt.d() + pl.q0 * mpK;
+  double* xt = pl.S().xt.d() + pl.q0 * mpK;
   if (pl.mode == 0) {
     launch_chain(mp, chain_args(pl, F, X, K, nullptr, 0), false, st);
     return;
@@ -1386,7 +1408,7 @@ void solve_backward(btd_plan& pl, const double* F, double* X, int64_t K, cudaStr
 // Single-device solve: forward -> interface RHS -> tree -> backward.
 void solve_device(btd_plan& pl, const double* F, double* X, int64_t K, cudaStream_t st) {
   const int64_t mp = pl.mp, m = pl.m, blk = pl.blk, mpK = mp * K, mK = m * K;
-  double* ft = pl.ft.d();
+  double* ft = pl.S().ft.d();
   pl.ev_mark(st);
   solve_forward(pl, F, X, K, ft, mpK, st);
   pl.ev_mark(st);
@@ -1414,53 +1436,54 @@ void solve_graphed(btd_plan& pl, const double* F, double* X, int64_t K, cudaStre
   }
   btd_plan::GraphEntry* ge = nullptr;
   for (auto& g : pl.graphs)
-    if (g.F == F && g.X == X && g.K == K) ge = &g;
+    if (g.F == F && g.X == X && g.K == K && g.slot == pl.cur) ge = &g;
   if (!ge) {
-    if (pl.graphs.size() >= 8) {  // bounded cache
+    if (pl.graphs.size() >= 24) {  // bounded cache (host pipeline: up to kHostBufs x kSlots keys)
       if (pl.graphs.front().exec) cudaGraphExecDestroy(pl.graphs.front().exec);
       pl.graphs.erase(pl.graphs.begin());
     }
-    pl.graphs.push_back({F, X, K, 0, nullptr, 0});
+    pl.graphs.push_back({F, X, K, pl.cur, 0, nullptr, 0});
     ge = &pl.graphs.back();
   }
   if (++ge->calls < 2) {
     solve_device(pl, F, X, K, st);
     return;
   }
-  if (!pl.own) {
-    CK(cudaStreamCreateWithFlags(&pl.own, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&pl.ev_in, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&pl.ev_out, cudaEventDisableTiming));
+  auto& S = pl.S();
+  if (!S.own) {
+    CK(cudaStreamCreateWithFlags(&S.own, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&S.ev_in, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&S.ev_out, cudaEventDisableTiming));
   }
   if (!ge->exec) {
     cudaGraph_t graph;
     const int64_t l0 = g_launches.load();
-    CK(cudaStreamBeginCapture(pl.own, cudaStreamCaptureModeThreadLocal));
+    CK(cudaStreamBeginCapture(S.own, cudaStreamCaptureModeThreadLocal));
     try {
-      solve_device(pl, F, X, K, pl.own);
+      solve_device(pl, F, X, K, S.own);
     } catch (...) {
-      cudaStreamEndCapture(pl.own, &graph);
+      cudaStreamEndCapture(S.own, &graph);
       throw;
     }
-    CK(cudaStreamEndCapture(pl.own, &graph));
+    CK(cudaStreamEndCapture(S.own, &graph));
     ge->nkern = g_launches.load() - l0;
     g_launches.fetch_sub(ge->nkern);  // counted when the graph runs, not when captured
     CK(cudaGraphInstantiate(&ge->exec, graph, 0));
     CK(cudaGraphDestroy(graph));
   }
-  CK(cudaEventRecord(pl.ev_in, st));
-  CK(cudaStreamWaitEvent(pl.own, pl.ev_in, 0));
-  CK(cudaGraphLaunch(ge->exec, pl.own));
+  CK(cudaEventRecord(S.ev_in, st));
+  CK(cudaStreamWaitEvent(S.own, S.ev_in, 0));
+  CK(cudaGraphLaunch(ge->exec, S.own));
   g_launches.fetch_add(ge->nkern);
-  CK(cudaEventRecord(pl.ev_out, pl.own));
-  CK(cudaStreamWaitEvent(st, pl.ev_out, 0));
+  CK(cudaEventRecord(S.ev_out, S.own));
+  CK(cudaStreamWaitEvent(st, S.ev_out, 0));
 }
 
 // Sharded phase A: local sweeps (base into f~), internal carries, and the carry of
 // the last owned range for the next rank (carry_out: mp x K, zero if none).
 void solve_shard_a(btd_plan& pl, const double* F, double* X, int64_t K, double* carry_out, cudaStream_t st) {
   const int64_t mp = pl.mp, m = pl.m, blk = pl.blk, mpK = mp * K, mK = m * K;
-  double* ft = pl.ft.d() + pl.q0 * mpK;
+  double* ft = pl.S().ft.d() + pl.q0 * mpK;
   CK(cudaMemsetAsync(carry_out, 0, (size_t)mpK * sizeof(double), st));
   pl.ev_mark(st);
   solve_forward(pl, F, X, K, ft, mpK, st);
@@ -1493,14 +1516,14 @@ __global__ void sum_ranks_kernel(const double* part_all, int world, int ncross, 
 // local series sums of nodes inside this rank, partial sums of crossing nodes.
 void solve_shard_b(btd_plan& pl, const double* carry_all, double* partial_out, int64_t K, cudaStream_t st) {
   const int64_t mp = pl.mp, mpK = mp * K;
-  double* ft = pl.ft.d();
+  double* ft = pl.S().ft.d();
   if (pl.rank >= 1) {
     add_block_kernel<<<64, 256, 0, st>>>(ft + pl.q0 * mpK, carry_all + (int64_t)(pl.rank - 1) * mpK, mpK);
     CK_LAUNCH();
   }
-  launch_gemm(mp, K, pl.nz, mk(pl.zbuf.d(), pl.z_id, 0, mpK, K), none(), 0.0,
+  launch_gemm(mp, K, pl.nz, mk(pl.S().zbuf.d(), pl.z_id, 0, mpK, K), none(), 0.0,
               {term(mk(pl.Rrows.d(), pl.z_roff, 0, 1, 0, pl.z_rld), mk(ft, pl.z_nlo, 0, mpK, K), 0, 1.0, pl.z_rld)}, st,
-              &pl.z_split);
+              split_with(pl.z_split, pl));
   launch_gemm(mp, K, pl.ncross, mk(partial_out, nullptr, 0, mpK, K), none(), 0.0,
               {term(mk(pl.Rrows.d(), pl.cross_roff, 0, 1, 0, pl.cross_ld), mk(ft, pl.cross_lo, 0, mpK, K), 0, 1.0,
                     pl.cross_k)},
@@ -1512,7 +1535,7 @@ void solve_shard_c(btd_plan& pl, const double* partial_all, const double* F, dou
   const int64_t mp = pl.mp, mpK = mp * K;
   if (pl.ncross) {
     dim3 grid((unsigned)std::min<int64_t>((mpK + 255) / 256, 64), (unsigned)std::min(pl.ncross, 65535));
-    sum_ranks_kernel<<<grid, 256, 0, st>>>(partial_all, pl.world, pl.ncross, mpK, pl.cross_node, pl.zbuf.d());
+    sum_ranks_kernel<<<grid, 256, 0, st>>>(partial_all, pl.world, pl.ncross, mpK, pl.cross_node, pl.S().zbuf.d());
     CK_LAUNCH();
   }
   solve_levels(pl, K, st);
@@ -1528,7 +1551,7 @@ int guarded(btd_plan* pl, void* stream, const std::function<void(cudaStream_t)>&
     DeviceGuard dg(pl->device);
     std::lock_guard<std::mutex> lk(pl->mu);
     cudaStream_t st = (cudaStream_t)stream;
-    if (pl->last_stream != st && pl->scratch_k) CK(cudaStreamSynchronize(pl->last_stream));
+    if (pl->last_stream != st && pl->sc[0].k) CK(cudaStreamSynchronize(pl->last_stream));
     pl->last_stream = st;
     fn(st);
   } catch (const BtdError& e) {
@@ -1672,31 +1695,57 @@ int btd_plan_solve(btd_plan* pl, const double* f, double* x, int64_t k, void* st
 }
 
 // Host-memory solve (the reference's numpy-in / numpy-out contract).  Columns are
-// independent, so the K columns run as equal chunks through a 3-stream pipeline:
+// independent, so the K columns run as equal chunks through a pipeline:
 // H2D of chunk c+1 (2-D strided copy out of the (n, m, k) layout) || solve of chunk c
-// || D2H of chunk c-1, with two device chunk buffers.  Needs pinned host memory to
+// || D2H of chunk c-1, with two device chunk buffers.  A narrow chunk does not fill
+// the GPU (c1: 64 columns = 72 chain CTAs), so consecutive chunks solve on two
+// compute streams with their own scratch slots.  Needs pinned host memory to
 // overlap (pageable memory still works, synchronously).
 int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int64_t k, void* stream) {
   if (!pl || !f_host || !x_host) { g_err = "NULL argument"; return BTD_ERR_INVALID_ARG; }
   if (k < 1) { g_err = "k must be >= 1"; return BTD_ERR_DIMENSION; }
   if (pl->world != 1) { g_err = "sharded plan: use btd_shard_solve_a/b/c"; return BTD_ERR_INVALID_ARG; }
   return guarded(pl, stream, [&](cudaStream_t st) {
-    // chunk width: an even divisor of k giving up to 4 chunks of >= 32 columns (>= 256 B rows)
+    // Column chunk plan.  Copies run on one H2D and one D2H stream (full duplex); the
+    // D2H pipe starts after H2D(chunk 0) + solve(chunk 0) and then streams, so chunks
+    // are narrow (>= 32 columns: >= 256 B rows still copy at full PCIe rate).  A
+    // narrow chunk's solve is latency-bound (each range is one chain of L steps
+    // whatever the width), so consecutive chunks solve concurrently on up to
+    // kSlots compute streams, each with its own scratch slot.
+    static int maxch = -1;
+    if (maxch < 0) {
+      const char* e = getenv("BTD_HOST_CHUNKS");
+      maxch = e ? std::max(1, std::min(btd_plan::kHostBufs, atoi(e))) : btd_plan::kHostBufs;
+    }
+    // measured (profiles/r01_host_pipeline.txt): 32-column chunks of a 256-column
+    // solve lose more to per-chunk solve latency than they gain in fill time
+    const int64_t minw = k >= 256 ? 64 : 32;
     int64_t kc = k;
-    for (int64_t nch : {4, 2})
-      if (k % nch == 0 && (k / nch) % 2 == 0 && k / nch >= 32) { kc = k / nch; break; }
+    for (int64_t nch = maxch; nch >= 2; --nch)
+      if (k % nch == 0 && (k / nch) % 2 == 0 && k / nch >= minw) { kc = k / nch; break; }
     const int64_t nch = k / kc, rows = pl->n * pl->m;
     const size_t celems = (size_t)rows * kc;
-    if (pl->hostio_k != kc) {
+    // concurrent solves: not with the cooperative tree kernel (two partially-resident
+    // cooperative grids could wait on each other) or while phase profiling (per-solve
+    // phase events are single-stream)
+    static int slots_env = -1;
+    if (slots_env < 0) {
+      const char* e = getenv("BTD_HOST_SLOTS");
+      slots_env = e ? std::max(1, std::min(btd_plan::kSlots, atoi(e))) : btd_plan::kSlots;
+    }
+    const int nstr = (pl->fused_tree || pl->profiling) ? 1 : (int)std::min<int64_t>(nch, slots_env);
+    if (pl->hostio_k != k) {
       for (auto& g : pl->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
       pl->graphs.clear();
-      pl->hostio_k = kc;
+      pl->hostio_k = k;
     }
-    if ((int64_t)celems > pl->hchunk_elems) {
-      pl->hchunk[0].alloc(celems * sizeof(double));
-      pl->hchunk[1].alloc(celems * sizeof(double));
-      pl->hchunk_elems = (int64_t)celems;
+    // up to kHostBufs chunks in flight: the H2D of chunk c waits only for the D2H of
+    // chunk c - kHostBufs (with two buffers the pipeline serialises in/solve/out)
+    const int nbuf = (int)std::min<int64_t>(nch, btd_plan::kHostBufs);
+    if ((int64_t)celems * nbuf > pl->hchunk_elems) {
+      pl->hchunk.alloc(celems * nbuf * sizeof(double));
+      pl->hchunk_elems = (int64_t)celems * nbuf;
       for (auto& g : pl->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
       pl->graphs.clear();
@@ -1704,32 +1753,77 @@ int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int6
     if (!pl->s_in) {
       CK(cudaStreamCreateWithFlags(&pl->s_in, cudaStreamNonBlocking));
       CK(cudaStreamCreateWithFlags(&pl->s_out, cudaStreamNonBlocking));
+      for (auto& x : pl->s_c) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
       for (auto& a : pl->ev_h)
         for (auto& e : a) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    ensure_scratch(*pl, kc);
+    struct SlotReset {
+      btd_plan* p;
+      ~SlotReset() { p->cur = 0; }
+    } reset{pl};
+    for (int sl = 0; sl < nstr; ++sl) {
+      pl->cur = sl;
+      ensure_scratch(*pl, kc);
+    }
+    const cudaStream_t cs[btd_plan::kSlots] = {st, pl->s_c[0], pl->s_c[1], pl->s_c[2]};
     cudaEvent_t start;
     CK(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
     CK(cudaEventRecord(start, st));
     CK(cudaStreamWaitEvent(pl->s_in, start, 0));
-    const size_t wbytes = (size_t)kc * sizeof(double), hpitch = (size_t)k * sizeof(double);
+    for (int i = 1; i < nstr; ++i) CK(cudaStreamWaitEvent(cs[i], start, 0));
+    const size_t hpitch = (size_t)k * sizeof(double);
+    // BTD_HOST_TRACE=1: per-chunk timeline (H2D / solve / D2H start+end) on stderr
+    static int trace = -1;
+    if (trace < 0) trace = getenv("BTD_HOST_TRACE") ? atoi(getenv("BTD_HOST_TRACE")) : 0;
+    std::vector<cudaEvent_t> tev;
+    auto tmark = [&](cudaStream_t s) {
+      if (!trace) return;
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      CK(cudaEventRecord(e, s));
+      tev.push_back(e);
+    };
+    tmark(st);
+    int64_t col = 0;
     for (int64_t c = 0; c < nch; ++c) {
-      const int b = (int)(c & 1);
-      double* dbuf = pl->hchunk[b].d();
+      const int b = (int)(c % nbuf), sl = (int)(c % nstr);
+      const size_t wbytes = (size_t)kc * sizeof(double);
+      const cudaStream_t cst = cs[sl];
+      double* dbuf = pl->hchunk.d() + (size_t)b * celems;
       cudaEvent_t in_done = pl->ev_h[b][0], comp_done = pl->ev_h[b][1], out_done = pl->ev_h[b][2];
-      if (c >= 2) CK(cudaStreamWaitEvent(pl->s_in, out_done, 0));  // buffer b free again
-      CK(cudaMemcpy2DAsync(dbuf, wbytes, f_host + c * kc, hpitch, wbytes, rows, cudaMemcpyHostToDevice, pl->s_in));
+      if (c >= nbuf) CK(cudaStreamWaitEvent(pl->s_in, out_done, 0));  // buffer b free again
+      tmark(pl->s_in);
+      CK(cudaMemcpy2DAsync(dbuf, wbytes, f_host + col, hpitch, wbytes, rows, cudaMemcpyHostToDevice, pl->s_in));
       CK(cudaEventRecord(in_done, pl->s_in));
-      CK(cudaStreamWaitEvent(st, in_done, 0));
-      solve_graphed(*pl, dbuf, dbuf, kc, st);
-      CK(cudaEventRecord(comp_done, st));
+      tmark(pl->s_in);
+      CK(cudaStreamWaitEvent(cst, in_done, 0));
+      pl->cur = sl;
+      tmark(cst);
+      solve_graphed(*pl, dbuf, dbuf, kc, cst);
+      CK(cudaEventRecord(comp_done, cst));
+      tmark(cst);
       CK(cudaStreamWaitEvent(pl->s_out, comp_done, 0));
-      CK(cudaMemcpy2DAsync(x_host + c * kc, hpitch, dbuf, wbytes, wbytes, rows, cudaMemcpyDeviceToHost, pl->s_out));
+      tmark(pl->s_out);
+      CK(cudaMemcpy2DAsync(x_host + col, hpitch, dbuf, wbytes, wbytes, rows, cudaMemcpyDeviceToHost, pl->s_out));
       CK(cudaEventRecord(out_done, pl->s_out));
+      tmark(pl->s_out);
+      col += kc;
     }
+    pl->cur = 0;
     CK(cudaStreamSynchronize(pl->s_out));
+    for (int i = 1; i < nstr; ++i) CK(cudaStreamSynchronize(cs[i]));
     CK(cudaStreamSynchronize(st));
     cudaEventDestroy(start);
+    if (trace) {
+      float ms[6];
+      fprintf(stderr, "[btd host] k=%lld chunks=%lld streams=%d\n", (long long)k, (long long)nch, nstr);
+      for (int64_t c = 0; c < nch; ++c) {
+        for (int i = 0; i < 6; ++i) CK(cudaEventElapsedTime(&ms[i], tev[0], tev[1 + 6 * c + i]));
+        fprintf(stderr, "  chunk %lld w=%lld  h2d %7.2f-%7.2f  solve %7.2f-%7.2f  d2h %7.2f-%7.2f\n", (long long)c,
+                (long long)kc, ms[0], ms[1], ms[2], ms[3], ms[4], ms[5]);
+      }
+      for (auto e : tev) cudaEventDestroy(e);
+    }
   });
 }
 
