@@ -87,6 +87,19 @@ int btd_plan_solve_host(btd_plan* plan, const double* f_host, double* x_host, in
 int btd_plan_destroy(btd_plan* plan);
 int btd_plan_query(const btd_plan* plan, btd_plan_info* info);
 
+/* ---- plan images (replaces ref io.py:125-203 write_plan/read_plan, DPLN) --
+ * btd_plan_export copies a finished plan (single or shard) into host memory:
+ * a 104-byte header (magic "BTDPLAN1", version, n, m, ranks, split, rank,
+ * world, sweep mode, padded order, three section sizes) followed by the raw
+ * device factor pool, the tree inverse rows and the E/H correction blocks.
+ * Call with dst = NULL to get the size in *nbytes.  btd_plan_import rebuilds
+ * the plan on `device` from such an image without redoing the preprocessing
+ * (the matrix is not needed; binding to a matrix is the caller's fingerprint
+ * check, as in ref io.py:157-160).  Errors: BTD_ERR_INVALID_ARG for a
+ * malformed image, BTD_ERR_UNSUPPORTED for another image version. */
+int btd_plan_export(btd_plan* plan, void* dst, int64_t* nbytes, void* stream);
+int btd_plan_import(const void* src, int64_t nbytes, int device, void* stream, btd_plan** out_plan);
+
 /* ---- row-sharded (multi-GPU) plans and solves --------------------------
  * The ranges (ranks*split of them, a multiple of `world`) are split
  * contiguously over `world` processes, one GPU each; rank r owns ranges

@@ -20,6 +20,11 @@ BTD_OK = 0
 BTD_ERR_DIMENSION = 1
 BTD_ERR_SINGULAR_PIVOT = 2
 BTD_ERR_INVALID_RANKS = 3
+BTD_ERR_CUDA = 4
+BTD_ERR_NCCL = 5
+BTD_ERR_OOM = 6
+BTD_ERR_INVALID_ARG = 7
+BTD_ERR_UNSUPPORTED = 8
 BTD_MATRIX_ON_DEVICE = 1
 
 # Every symbol include/blocktri_b200.h declares (checked by tests/test_abi.py).
@@ -29,6 +34,8 @@ EXPORTS = (
     "btd_plan_solve_host",
     "btd_plan_destroy",
     "btd_plan_query",
+    "btd_plan_export",
+    "btd_plan_import",
     "btd_plan_create_shard",
     "btd_shard_contrib",
     "btd_shard_finish",
@@ -80,6 +87,10 @@ def load():
     lib.btd_plan_destroy.restype = i32
     lib.btd_plan_query.argtypes = [vp, ctypes.POINTER(PlanInfo)]
     lib.btd_plan_query.restype = i32
+    lib.btd_plan_export.argtypes = [vp, vp, ctypes.POINTER(i64), vp]
+    lib.btd_plan_export.restype = i32
+    lib.btd_plan_import.argtypes = [vp, i64, i32, vp, ctypes.POINTER(vp)]
+    lib.btd_plan_import.restype = i32
     lib.btd_plan_create_shard.argtypes = [dp, dp, dp, i64, i64, i64, i64, i32, i32, i32, i32, vp,
                                           ctypes.POINTER(vp), ctypes.POINTER(i64)]
     lib.btd_plan_create_shard.restype = i32

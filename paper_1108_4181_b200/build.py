@@ -22,7 +22,7 @@ OUT = os.path.join(PKG, "_lib", "libblocktri_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [
-    "-shared", "-Xcompiler", "-fPIC", "-std=c++17", "-O3", "-lineinfo",
+    "-shared", "-Xcompiler", "-fPIC,-Wshadow", "-std=c++17", "-O3", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-diag-suppress", "177",
 ]

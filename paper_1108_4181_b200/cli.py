@@ -9,9 +9,11 @@ reference (defaults <- JSON config or an emitted report <- flags, unknown keys
 rejected, cli.py:96-150) and so do the exit codes (0 ok, 1 numerical,
 2 i/o, 3 config; errors as one JSON line on stderr, cli.py:449-467).
 
-``plan_cache`` is accepted for compatibility; the reference's DPLN container
-stores its LU/superposition factor set, which the GPU plan does not use, so
-the GPU plan is rebuilt (preprocessing is seconds on the device).
+``plan_cache`` follows ref cli.py:183-196: an existing DPLN file bound to this
+matrix (and the same ranks/split) is loaded instead of building, anything else
+(missing, other matrix, malformed) is rebuilt and the cache rewritten.  GPU plan
+files import the device factors directly (io.read_plan); the reference's own
+CPU DPLN files are validated and the GPU plan is rebuilt from the matrix.
 
     python -m paper_1108_4181_b200.cli solve --matrix A.btr --rhs f.bvc --ranks 8 [--split 4]
 """
@@ -95,7 +97,20 @@ def cmd_solve(cfg):
         if v.n != matrix.n or v.m != matrix.m:
             raise ConfigError(f"rhs layout ({v.n},{v.m}) != matrix ({matrix.n},{matrix.m})")
     t0 = time.time()
-    plan = dichotomy.plan_build(matrix, cfg["ranks"], split=cfg["split"])
+    plan, cache, cache_hit = None, cfg.get("plan_cache"), False
+    if cache and os.path.exists(cache):
+        try:
+            plan = bio.read_plan(cache, matrix)
+            if plan.ranks != cfg["ranks"] or plan.split != cfg["split"]:
+                plan = None
+            else:
+                cache_hit = True
+        except bio.FileFormatError:
+            plan = None
+    if plan is None:
+        plan = dichotomy.plan_build(matrix, cfg["ranks"], split=cfg["split"])
+        if cache:
+            bio.write_plan(cache, plan)
     build_s = time.time() - t0
     batch = np.stack([v.data for v in vectors], axis=2)
     t0 = time.time()
@@ -113,7 +128,8 @@ def cmd_solve(cfg):
     worst = max(residuals)
     results = {"residual": worst, "residuals": residuals, "plan_build_seconds": build_s,
                "solve_seconds": solve_s, "ranks": cfg["ranks"], "stages": stage_count(cfg["ranks"]),
-               "solutions": sols, "backend": "b200", "device_ranges": plan.nranges}
+               "solutions": sols, "backend": "b200", "device_ranges": plan.nranges,
+               "plan_cache_hit": cache_hit}
     report = {"command": "solve", "config": cfg, "results": results}
     bio.atomic_write(os.path.join(out, "solve_report.json"),
                      (json.dumps(report, indent=2, sort_keys=True) + "\n").encode())

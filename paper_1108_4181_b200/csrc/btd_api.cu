@@ -663,12 +663,15 @@ int64_t pad_order(int64_t m, int mode) {
 // Ranges owned by this rank: [q0, q1).  The rank reads only its rows of the
 // matrix and produces its factors plus the four reduced-system contributions
 // per range; the tree part (build_finish) needs everyone's contributions.
+//
+// restore >= 0: metadata only (plan import, btd_plan_import); the factor pool is
+// loaded from an exported image afterwards and `restore` is the image's sweep mode.
 void build_local(btd_plan& pl, const double* diag, const double* lower, const double* upper, int flags,
-                 cudaStream_t st, int64_t* err_row, int64_t* err_range) {
+                 cudaStream_t st, int64_t* err_row, int64_t* err_range, int restore = -1) {
   const int64_t n = pl.n, m = pl.m;
   int forced = -1;
   if (const char* e = getenv("BTD_FORCE_MODE")) forced = atoi(e);
-  pl.mode = forced >= 0 ? forced : (m > 256 ? 1 : 0);
+  pl.mode = restore >= 0 ? restore : forced >= 0 ? forced : (m > 256 ? 1 : 0);
   pl.mp = pad_order(m, pl.mode);
   const int64_t mp = pl.mp, blk = mp * mp;
   pl.blk = blk;
@@ -703,8 +706,8 @@ void build_local(btd_plan& pl, const double* diag, const double* lower, const do
   // ---- local padded matrix rows [R0, R0+nl): [C | Lw | Uw], nl blocks each
   //      Lw[i] = lower[R0+i] (couples row R0+i+1 to R0+i), Uw[i] = upper[R0+i]; zero / identity past n
   DevBuf mat, tmp;
-  mat.alloc((size_t)3 * nl * blk * sizeof(double));
-  {
+  if (restore < 0) {
+    mat.alloc((size_t)3 * nl * blk * sizeof(double));
     const double* srcs[3] = {diag, lower, upper};
     const int64_t counts[3] = {std::max<int64_t>(0, std::min(nl, n - R0)), std::max<int64_t>(0, std::min(nl, n - 1 - R0)),
                                std::max<int64_t>(0, std::min(nl, n - 1 - R0))};
@@ -755,6 +758,7 @@ void build_local(btd_plan& pl, const double* diag, const double* lower, const do
   CK_LAUNCH();
   pl.factor_bytes = (int64_t)o * blk * sizeof(double);
 
+  if (restore < 0) {
   double* pool = pl.pool.d();
   const int64_t* lo_arr = pl.d_lo;
   const int64_t* slot_arr = pl.d_slot0;
@@ -876,6 +880,7 @@ void build_local(btd_plan& pl, const double* diag, const double* lower, const do
                 {term(mk(pool, d_c1a, 0, blk, mp), mk(pool, pl.upload(c2b), 0, blk, mp), mp)}, st);
     launch_gemm(mp, mp, nb, mk(cb, pl.upload(c3c), 0, blk, mp), mk(pool, pl.upload(c3in), 0, blk, mp), 1.0, {}, st);
   }
+  }  // restore < 0
   mat.release();
 
   // ---- solve-time local batches
@@ -961,12 +966,12 @@ void build_splits(btd_plan& pl) {
 
 // ---------------------------------------------------------------- plan build, global part
 // contrib_all: [nr][4][mp][mp] device, identical on every rank.
-void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int64_t* err_row) {
+void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int64_t* err_row, bool restore = false) {
   const int64_t mp = pl.mp, blk = pl.blk, nr = pl.nr;
   double* pool = pl.pool.d();
   const double* I = pool + pl.off_I * blk;
   // reduced system: Rd_q = c0_q - c1_{q-1}, Rl_{q-1} = c2_{q-1}, Ru_q = c3_q
-  {
+  if (!restore) {
     std::vector<int64_t> d_c, d_in, d_a, l_c, l_in, u_c, u_in;
     for (int64_t q = 0; q < nr; ++q) {
       if (q >= 1) { d_c.push_back(pl.off_Rd + q); d_in.push_back(4 * q); d_a.push_back(4 * (q - 1) + 1); }
@@ -1015,13 +1020,16 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
   }
   eoff[nn] = rtot;
   DevBuf tp, tfs, tfc, ws;
-  const int64_t tpD = 0, tpS = tot, tpAD = 2 * tot, tpY = 3 * tot, tpDt = 4 * tot;
+  double* T = nullptr;
+  const int64_t tpY = 3 * tot;
+  if (!restore) {
+  const int64_t tpD = 0, tpS = tot, tpAD = 2 * tot, tpDt = 4 * tot;
   tp.alloc((size_t)(4 * tot + nn) * blk * sizeof(double));
   CK(cudaMemsetAsync(tp.p, 0, (size_t)(4 * tot + nn) * blk * sizeof(double), st));
   tfs.alloc(sizeof(int32_t) * nn);
   tfc.alloc(sizeof(int32_t) * nn);
   CK(cudaMemsetAsync(tfs.p, 0xff, sizeof(int32_t) * nn, st));
-  double* T = tp.d();
+  T = tp.d();
   for (int64_t lev = 0; lev <= maxlevel; ++lev) {
     std::vector<int> ids;
     int64_t smax = 0;
@@ -1102,9 +1110,10 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
         fail(BTD_ERR_SINGULAR_PIVOT, buf);
       }
   }
+  }  // !restore
   // R rows, then E = R[:, :mp] Rl_{lo-1}, H = R[:, -mp:] Ru_{hi}
   pl.Rrows.alloc((size_t)rtot * sizeof(double));
-  {
+  if (!restore) {
     std::vector<int64_t> ynb0(nn);
     for (int b = 0; b < nn; ++b) ynb0[b] = tpY + nb0[b];
     assemble_rows_kernel<<<1184, 256, 0, st>>>(T, pl.upload(ynb0), pl.upload(roff), pl.upload(sz), pl.upload(eoff), nn,
@@ -1114,8 +1123,8 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
   pl.d_roff = pl.upload(roff);
   pl.d_rld = pl.upload(rld);
   pl.EH.alloc((size_t)2 * nn * blk * sizeof(double));
-  CK(cudaMemsetAsync(pl.EH.p, 0, (size_t)2 * nn * blk * sizeof(double), st));
-  {
+  if (!restore) {
+    CK(cudaMemsetAsync(pl.EH.p, 0, (size_t)2 * nn * blk * sizeof(double), st));
     std::vector<int64_t> ec, ea, eld, eb, hc, ha, hld, hb;
     for (int b = 0; b < nn; ++b) {
       const Node& nd = pl.nodes[b];
@@ -1825,6 +1834,86 @@ int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int6
       for (auto e : tev) cudaEventDestroy(e);
     }
   });
+}
+
+// ---- plan image: header + factor pool + inverse rows + E/H blocks (device bytes).
+// The metadata (ranges, tree, batches) is recomputed from the header on import;
+// the factors are the output of the expensive sequential preprocessing.
+namespace {
+constexpr int64_t kImageMagic = 0x314e414c50445442LL;  // "BTDPLAN1" little-endian
+constexpr int64_t kImageVersion = 1;
+struct ImageHeader {
+  int64_t magic, version, n, m, ranks, split, rank, world, mode, mp, pool_bytes, rrows_bytes, eh_bytes;
+};
+}  // namespace
+
+int btd_plan_export(btd_plan* pl, void* dst, int64_t* nbytes, void* stream) {
+  if (!pl || !nbytes) { g_err = "btd_plan_export: NULL argument"; return BTD_ERR_INVALID_ARG; }
+  if (!pl->finished) { g_err = "btd_plan_export: plan not finished"; return BTD_ERR_INVALID_ARG; }
+  const int64_t need = (int64_t)(sizeof(ImageHeader) + pl->pool.bytes + pl->Rrows.bytes + pl->EH.bytes);
+  if (!dst) { *nbytes = need; return BTD_OK; }
+  if (*nbytes < need) { g_err = "btd_plan_export: destination too small"; return BTD_ERR_INVALID_ARG; }
+  *nbytes = need;
+  return guarded(pl, stream, [&](cudaStream_t st) {
+    ImageHeader h{kImageMagic, kImageVersion, pl->n, pl->m, pl->ranks, pl->split, pl->rank, pl->world,
+                  pl->mode, pl->mp, (int64_t)pl->pool.bytes, (int64_t)pl->Rrows.bytes, (int64_t)pl->EH.bytes};
+    char* out = static_cast<char*>(dst);
+    memcpy(out, &h, sizeof h);
+    out += sizeof h;
+    CK(cudaMemcpyAsync(out, pl->pool.p, pl->pool.bytes, cudaMemcpyDeviceToHost, st));
+    out += pl->pool.bytes;
+    CK(cudaMemcpyAsync(out, pl->Rrows.p, pl->Rrows.bytes, cudaMemcpyDeviceToHost, st));
+    out += pl->Rrows.bytes;
+    CK(cudaMemcpyAsync(out, pl->EH.p, pl->EH.bytes, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int btd_plan_import(const void* src, int64_t nbytes, int device, void* stream, btd_plan** out_plan) {
+  g_err.clear();
+  if (!src || !out_plan) { g_err = "btd_plan_import: NULL argument"; return BTD_ERR_INVALID_ARG; }
+  *out_plan = nullptr;
+  ImageHeader h;
+  if (nbytes < (int64_t)sizeof h) { g_err = "plan image: truncated header"; return BTD_ERR_INVALID_ARG; }
+  memcpy(&h, src, sizeof h);
+  if (h.magic != kImageMagic) { g_err = "plan image: bad magic"; return BTD_ERR_INVALID_ARG; }
+  if (h.version != kImageVersion) { g_err = "plan image: unsupported version"; return BTD_ERR_UNSUPPORTED; }
+  if (h.n < 1 || h.m < 1 || h.ranks < 1 || h.ranks > h.n || h.split < 1 || h.world < 1 || h.rank < 0 ||
+      h.rank >= h.world || (h.mode != 0 && h.mode != 1) || h.pool_bytes < 0 || h.rrows_bytes < 0 || h.eh_bytes < 0 ||
+      nbytes != (int64_t)sizeof h + h.pool_bytes + h.rrows_bytes + h.eh_bytes) {
+    g_err = "plan image: inconsistent header or size";
+    return BTD_ERR_INVALID_ARG;
+  }
+  auto* pl = new btd_plan();
+  pl->device = device;
+  pl->n = h.n; pl->m = h.m; pl->ranks = h.ranks; pl->split = h.split;
+  pl->rank = (int)h.rank; pl->world = (int)h.world;
+  try {
+    DeviceGuard dg(device);
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t row = -1, rng = -1;
+    build_local(*pl, nullptr, nullptr, nullptr, 0, st, &row, &rng, (int)h.mode);
+    if (pl->mp != h.mp || (int64_t)pl->pool.bytes != h.pool_bytes) fail(BTD_ERR_INVALID_ARG, "plan image: pool layout mismatch");
+    const char* in = static_cast<const char*>(src) + sizeof h;
+    CK(cudaMemcpyAsync(pl->pool.p, in, h.pool_bytes, cudaMemcpyHostToDevice, st));
+    in += h.pool_bytes;
+    build_finish(*pl, nullptr, st, &row, true);
+    if ((int64_t)pl->Rrows.bytes != h.rrows_bytes || (int64_t)pl->EH.bytes != h.eh_bytes)
+      fail(BTD_ERR_INVALID_ARG, "plan image: tree layout mismatch");
+    CK(cudaMemcpyAsync(pl->Rrows.p, in, h.rrows_bytes, cudaMemcpyHostToDevice, st));
+    in += h.rrows_bytes;
+    CK(cudaMemcpyAsync(pl->EH.p, in, h.eh_bytes, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  } catch (const BtdError& e) {
+    delete pl;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    delete pl;
+    return BTD_ERR_CUDA;
+  }
+  *out_plan = pl;
+  return BTD_OK;
 }
 
 int btd_plan_destroy(btd_plan* pl) {

@@ -63,6 +63,31 @@ def _resolve_device(device):
     return int(device)
 
 
+def build_partition_tree(count):
+    """Algorithm 1's partition tree over ``count`` reduced blocks, BFS order.
+
+    Same node list as ref dichotomy.py:28-57: queue from (0, count-1), split at
+    k = lo + (hi - lo + 1) // 2, children (lo, k-1) and (k+1, hi) when non-empty.
+    Returns [(lo, hi, k, level)].  (The device plan builds the same tree in C++,
+    btd_api.cu partition_tree.)"""
+    nodes, queue = [], [(0, count - 1, 0)] if count > 0 else []
+    head = 0
+    while head < len(queue):
+        lo, hi, level = queue[head]
+        head += 1
+        k = lo + (hi - lo + 1) // 2
+        nodes.append((lo, hi, k, level))
+        if k - 1 >= lo:
+            queue.append((lo, k - 1, level + 1))
+        if hi >= k + 1:
+            queue.append((k + 1, hi, level + 1))
+    return nodes
+
+
+def tree_node_sizes(count):
+    return [hi - lo + 1 for lo, hi, _k, _lev in build_partition_tree(count)]
+
+
 class DevicePlan:
     """Preprocessing product bound to one matrix (mirrors ref DichotomyPlan,
     dichotomy.py:99-131).  Factors live in HBM of ``device``."""

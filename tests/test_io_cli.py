@@ -66,3 +66,40 @@ def test_cli_solve_end_to_end(tmp_path):
     import blocktri_oracle as O
     ref = O.plan_solve(O.plan_build(d, lo, up, 4), f)
     assert O.max_rel_err(x0, ref[:, :, 0]) <= 1e-9
+
+
+# ---- DPLN plan containers (ref io.py:125-203) ------------------------------------
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+REF_BTR = os.path.join(GOLDEN, "ref_plan_p3.btr")
+REF_DPLN = os.path.join(GOLDEN, "ref_plan_p3.dpln")  # written by the reference (make_ref_plan.py)
+
+
+def test_reference_dpln_header_and_binding(monkeypatch):
+    from paper_1108_4181_b200 import dichotomy
+
+    matrix = bio.read_matrix(REF_BTR)
+    calls = []
+    monkeypatch.setattr(dichotomy, "plan_build", lambda m, ranks, **kw: calls.append((m.n, m.m, ranks)) or "plan")
+    assert bio.read_plan(REF_DPLN, matrix) == "plan"  # payload length matched the reference's file
+    assert calls == [(37, 3, 5)]
+    raw = open(REF_DPLN, "rb").read()
+    n, m, ranks, L, npad = struct.unpack("<QQQQQ", raw[12:52])
+    assert (n, m, ranks, L, npad) == (37, 3, 5, 8, 40)
+    assert len(raw) - 60 - struct.unpack("<Q", raw[52:60])[0] == bio._ref_plan_payload_bytes(n, m, ranks, L)
+
+
+def test_dpln_rejections(tmp_path, monkeypatch):
+    from paper_1108_4181_b200 import dichotomy
+
+    monkeypatch.setattr(dichotomy, "plan_build", lambda *a, **k: "plan")
+    matrix = bio.read_matrix(REF_BTR)
+    raw = open(REF_DPLN, "rb").read()
+    p = tmp_path / "x.dpln"
+    for bad, what in [(b"XPLN" + raw[4:], "magic"), (raw[:4] + struct.pack("<Q", 7) + raw[12:], "version"),
+                      (raw[:-8], "truncated"), (raw + b"\0", "trailing")]:
+        p.write_bytes(bad)
+        with pytest.raises(bio.FileFormatError):
+            bio.read_plan(p, matrix)
+    d, lo, up, _ = configs.dominant_numpy(37, 3, 1, seed=99)  # another matrix
+    with pytest.raises(bio.FileFormatError, match="does not belong"):
+        bio.read_plan(REF_DPLN, BlockTriMatrix(d, lo, up))
