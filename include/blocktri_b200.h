@@ -98,6 +98,21 @@ int btd_plan_query(const btd_plan* plan, btd_plan_info* info);
  * check, as in ref io.py:157-160).  Errors: BTD_ERR_INVALID_ARG for a
  * malformed image, BTD_ERR_UNSUPPORTED for another image version. */
 int btd_plan_export(btd_plan* plan, void* dst, int64_t* nbytes, void* stream);
+
+/* ---- band route (ref bands.py) ---------------------
+ * Band storage: bands[k*n + j] = a(j + k - d, j), k = 0..2d (ref bands.py:18-41).
+ * btd_band_to_blocktri replaces ref bands.py:120-157 band_as_blocktrid: block
+ *   order m >= d, nb = ceil(n/m) blocks; writes diag (nb,m,m), lower/upper
+ *   (nb-1,m,m) with the reference's signs and identity padding.  Device pointers.
+ *   BTD_ERR_DIMENSION when m < d (ref BlockTooSmall) or n < 1.
+ * btd_band_from_probes replaces ref bands.py:94-117 probing_build (+ the
+ *   symmetrization at bands.py:73-84): y = A * P, P the n x (2d+1) class-probe
+ *   matrix P[i][c] = (i mod (2d+1) == c), row-major with leading dimension ldy;
+ *   writes the symmetrized band (B + B^T)/2.  BTD_ERR_DIMENSION when 2d+1 > n
+ *   (ref BandTooWide).  Device pointers; both are stream-ordered. */
+int btd_band_to_blocktri(const double* bands, int64_t n, int64_t d, int64_t m, double* diag, double* lower,
+                         double* upper, void* stream);
+int btd_band_from_probes(const double* y, int64_t n, int64_t d, int64_t ldy, double* bands, void* stream);
 int btd_plan_import(const void* src, int64_t nbytes, int device, void* stream, btd_plan** out_plan);
 
 /* ---- row-sharded (multi-GPU) plans and solves --------------------------

@@ -36,6 +36,8 @@ EXPORTS = (
     "btd_plan_query",
     "btd_plan_export",
     "btd_plan_import",
+    "btd_band_to_blocktri",
+    "btd_band_from_probes",
     "btd_plan_create_shard",
     "btd_shard_contrib",
     "btd_shard_finish",
@@ -91,6 +93,10 @@ def load():
     lib.btd_plan_export.restype = i32
     lib.btd_plan_import.argtypes = [vp, i64, i32, vp, ctypes.POINTER(vp)]
     lib.btd_plan_import.restype = i32
+    lib.btd_band_to_blocktri.argtypes = [dp, i64, i64, i64, dp, dp, dp, vp]
+    lib.btd_band_to_blocktri.restype = i32
+    lib.btd_band_from_probes.argtypes = [dp, i64, i64, i64, dp, vp]
+    lib.btd_band_from_probes.restype = i32
     lib.btd_plan_create_shard.argtypes = [dp, dp, dp, i64, i64, i64, i64, i32, i32, i32, i32, vp,
                                           ctypes.POINTER(vp), ctypes.POINTER(i64)]
     lib.btd_plan_create_shard.restype = i32

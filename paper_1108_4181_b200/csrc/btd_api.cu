@@ -40,6 +40,7 @@
 #include "btd_chain.cuh"
 #include "btd_gemm.cuh"
 #include "btd_inv.cuh"
+#include "btd_band.cuh"
 #include "btd_tree.cuh"
 
 using namespace btd;
@@ -1614,6 +1615,41 @@ int create_impl(const double* diag, const double* lower, const double* upper, in
 extern "C" {
 
 int btd_version(void) { return 1; }
+
+int btd_band_to_blocktri(const double* bands, int64_t n, int64_t d, int64_t m, double* diag, double* lower,
+                         double* upper, void* stream) {
+  g_err.clear();
+  if (n < 1 || d < 0 || m < 1) { g_err = "band: need n >= 1, d >= 0, m >= 1"; return BTD_ERR_DIMENSION; }
+  if (m < d) { g_err = "band: block order smaller than the half-bandwidth"; return BTD_ERR_DIMENSION; }
+  const int64_t nb = (n + m - 1) / m;
+  if (!bands || !diag || (nb > 1 && (!lower || !upper))) { g_err = "band: NULL pointer"; return BTD_ERR_INVALID_ARG; }
+  try {
+    const int64_t total = (3 * nb - 2) * m * m;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    band_to_blocks_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(bands, n, d, m, nb, diag, lower, upper);
+    CK_LAUNCH();
+  } catch (const BtdError& e) {
+    return e.code;
+  }
+  return BTD_OK;
+}
+
+int btd_band_from_probes(const double* y, int64_t n, int64_t d, int64_t ldy, double* bands, void* stream) {
+  g_err.clear();
+  if (n < 1 || d < 0) { g_err = "band: need n >= 1 and d >= 0"; return BTD_ERR_DIMENSION; }
+  if (2 * d + 1 > n) { g_err = "band: 2d+1 exceeds the operator order"; return BTD_ERR_DIMENSION; }
+  if (ldy < 2 * d + 1) { g_err = "band: ldy < 2d+1"; return BTD_ERR_INVALID_ARG; }
+  if (!y || !bands) { g_err = "band: NULL pointer"; return BTD_ERR_INVALID_ARG; }
+  try {
+    const int64_t total = (2 * d + 1) * n;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    band_from_probes_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(y, n, d, ldy, bands);
+    CK_LAUNCH();
+  } catch (const BtdError& e) {
+    return e.code;
+  }
+  return BTD_OK;
+}
 int64_t btd_launch_count(void) { return g_launches.load(); }
 const char* btd_last_error(void) { return g_err.c_str(); }
 

@@ -1,0 +1,60 @@
+// Band route: band storage <-> block-tridiagonal blocks,
+// and band recovery from probe responses.  Pure data movement / one add per
+// entry: HBM-bound, every output element computed by one thread from at most
+// two gathered inputs (no staging needed; the outputs are written coalesced).
+//
+// Band storage (ref bands.py:18-41): bands[k][j] = a(j + k - d, j), k = 0..2d.
+#pragma once
+#include <cstdint>
+
+namespace btd {
+
+// band_as_blocktrid (ref bands.py:120-157): block order m >= d, nb = ceil(n/m)
+// blocks; diag[b] = a(bm+r, bm+c), lower[b] = -a((b+1)m+r, bm+c),
+// upper[b] = -a(bm+r, (b+1)m+c); padding rows g >= n get diag 1.  Entries
+// outside the band stay +0.0 (in-band zeros become -0.0 on the couplings,
+// like the reference's `-v`).
+__global__ void band_to_blocks_kernel(const double* __restrict__ bands, int64_t n, int64_t d, int64_t m,
+                                      int64_t nb, double* __restrict__ diag, double* __restrict__ lower,
+                                      double* __restrict__ upper) {
+  const int64_t mm = m * m, nd = nb * mm, nc = (nb - 1) * mm, total = nd + 2 * nc;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t which, b, rc;
+    if (e < nd) { which = 0; b = e / mm; rc = e % mm; }
+    else if (e < nd + nc) { which = 1; b = (e - nd) / mm; rc = (e - nd) % mm; }
+    else { which = 2; b = (e - nd - nc) / mm; rc = (e - nd - nc) % mm; }
+    const int64_t r = rc / m, c = rc % m;
+    const int64_t i = (which == 1 ? b + 1 : b) * m + r;
+    const int64_t j = (which == 2 ? b + 1 : b) * m + c;
+    const int64_t off = i - j;
+    double v = 0.0;
+    if (i < n && j < n && off >= -d && off <= d) {
+      const double a = bands[(d + off) * n + j];
+      v = which == 0 ? a : -a;
+    } else if (which == 0 && i == j && i >= n) {
+      v = 1.0;
+    }
+    double* out = which == 0 ? diag : which == 1 ? lower : upper;
+    out[b * mm + rc] = v;
+  }
+}
+
+// probing_build + symmetrized (ref bands.py:94-117, 73-84): y is the n x w
+// response matrix (row-major, leading dimension ldy) to the w = 2d+1 class probes
+// p_c = [i mod w == c].  raw(k, j) = y[j + k - d][j mod w]; the result is
+// 0.5 * (raw(k, j) + raw(2d - k, j + k - d)) = 0.5 * (y[j+off][j mod w] + y[j][(j+off) mod w])
+// for 0 <= j, j + off < n (off = k - d), else 0.
+__global__ void band_from_probes_kernel(const double* __restrict__ y, int64_t n, int64_t d, int64_t ldy,
+                                        double* __restrict__ bands) {
+  const int64_t w = 2 * d + 1, total = w * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / n, j = e % n, off = k - d, i = j + off;
+    double v = 0.0;
+    if (i >= 0 && i < n) v = 0.5 * (y[i * ldy + j % w] + y[j * ldy + i % w]);
+    bands[e] = v;
+  }
+}
+
+}  // namespace btd

@@ -42,6 +42,26 @@ class InconsistentRanges(BlocktriError):
     """Ranges do not tile the matrix (ref errors.py:36)."""
 
 
+class DeadlockDetected(BlocktriError):
+    """A rank waits on a message no rank will send (ref errors.py:40)."""
+
+
+class StageViolation(BlocktriError):
+    """An execution trace violates the dichotomy stage structure (ref errors.py:44)."""
+
+
+class Breakdown(BlocktriError):
+    """Conjugate-gradient breakdown (ref errors.py:56)."""
+
+
+class BandTooWide(BlocktriError):
+    """Probing bandwidth does not fit the operator order (ref errors.py:60)."""
+
+
+class BlockTooSmall(BlocktriError):
+    """Block order smaller than the band half-width (ref errors.py:64)."""
+
+
 class DeviceError(BlocktriError):
     """CUDA / NCCL failure or missing native library (no reference analogue:
     the reference never leaves the host)."""
@@ -50,7 +70,8 @@ class DeviceError(BlocktriError):
 _BY_NAME = {
     c.__name__: c
     for c in (BlocktriError, DimensionMismatch, SingularBlock, SingularPivot,
-              IndexOutOfRange, InvalidRankCount, InconsistentRanges, DeviceError)
+              IndexOutOfRange, InvalidRankCount, InconsistentRanges, DeadlockDetected,
+              StageViolation, Breakdown, BandTooWide, BlockTooSmall, DeviceError)
 }
 
 
