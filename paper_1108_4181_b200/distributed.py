@@ -186,23 +186,58 @@ class ShardedPlan:
             raise _err.InvalidRankCount("invalid rank count")
         raise _err.DeviceError(f"shard plan build failed on rank {first} with status {code0}")
 
-    def solve(self, f_local, out=None):
+    def _gather(self, out, inp, label, trace, slot_bytes, cap_bytes):
+        """One all-gather; with a trace, log its logical dissemination stages and
+        its measured duration (CUDA events on the current stream, else wall clock)."""
+        if trace is None:
+            self.dist.all_gather_into_tensor(out, inp, group=self.group)
+            return
+        from .trace import allgather_schedule
+
+        cuda = getattr(inp, "is_cuda", False)
+        if cuda:
+            import torch
+
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        else:
+            import time
+
+            t0 = time.perf_counter()
+        self.dist.all_gather_into_tensor(out, inp, group=self.group)
+        if cuda:
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+        else:
+            ms = (time.perf_counter() - t0) * 1e3
+        allgather_schedule(trace, self.world, slot_bytes, cap_bytes, trace.stages)
+        trace.timings.append((label, ms))
+
+    def solve(self, f_local, out=None, trace=None):
         """f_local: (row_hi - row_lo, m, K) rows of this shard -> x_local
-        (written into ``out`` when given; may alias f_local)."""
+        (written into ``out`` when given; may alias f_local).  ``trace``: an
+        :class:`~.trace.ExecutionTrace` (nranks = world) that receives the logical
+        stages and measured times of the two exchanges."""
         k = int(f_local.shape[2])
         x_local = f_local.new_empty(f_local.shape) if out is None else out
         nc, npart = self.be.exchange_size(self.h, k)
+        cap = (self.m * self.m + self.m) * 8 * k  # ref harness.py:166-180 message cap
         carry = self.be.empty(nc)
         self.be.solve_a(self.h, f_local, x_local, k, carry)
         carry_all = self.be.empty(nc * self.world)
-        self.dist.all_gather_into_tensor(carry_all, carry, group=self.group)
+        self._gather(carry_all, carry, "carry", trace, nc * 8, cap)
         part = self.be.empty(max(npart, 1))
         self.be.solve_b(self.h, carry_all, part, k)
         part_all = self.be.empty(max(npart, 1) * self.world)
         if npart:
-            self.dist.all_gather_into_tensor(part_all, part[:npart], group=self.group)
+            self._gather(part_all, part[:npart], "partial", trace, npart * 8, cap)
         self.be.solve_c(self.h, part_all, f_local, x_local, k)
         return x_local
+
+    def collectives_per_solve(self, k=1):
+        """1 (carry) or 2 (carry + crossing-node partial sums) all-gathers per solve."""
+        return 1 + (self.be.exchange_size(self.h, k)[1] > 0)
 
     def close(self):
         if getattr(self, "h", None) is not None:

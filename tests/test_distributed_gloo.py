@@ -47,8 +47,12 @@ def _worker(rank, world, port, case, q):
         except Exception as exc:  # noqa: BLE001
             q.put((rank, "error", type(exc).__name__, getattr(exc, "row", None)))
             return
-        xl = plan.solve(torch.from_numpy(np.ascontiguousarray(f[plan.row_lo:plan.row_hi])))
-        q.put((rank, "ok", plan.row_lo, plan.row_hi, xl.numpy()))
+        from paper_1108_4181_b200.trace import ExecutionTrace
+
+        tr = ExecutionTrace(world)
+        xl = plan.solve(torch.from_numpy(np.ascontiguousarray(f[plan.row_lo:plan.row_hi])), trace=tr)
+        q.put((rank, "ok", plan.row_lo, plan.row_hi, xl.numpy(), tr.records, tr.timings,
+               plan.collectives_per_solve(k)))
     finally:
         dist.destroy_process_group()
 
@@ -94,3 +98,30 @@ def test_world2_singular_pivot_raised_on_every_rank():
 
 def test_stage_law():
     assert [stage_count(p) for p in (1, 2, 3, 4, 6, 8, 64, 256)] == [0, 1, 2, 2, 3, 3, 6, 8]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_solve_trace_stage_law_and_volume(world):
+    """Row f4: the sharded solve's logical trace has collectives*ceil(log2 W) stages,
+    every rank logs the same schedule, each all-gather moves W(W-1) slots."""
+    from paper_1108_4181_b200.trace import CostModelParams, ExecutionTrace, audit_trace
+
+    case = dict(n=200, m=3, k=2, ranks=8, split=2, seed=7)
+    res = _run(case, world=world)
+    assert all(r[1] == "ok" for r in res), res
+    recs, ncoll = res[0][5], res[0][7]
+    assert all(r[5] == recs for r in res) and all(r[7] == ncoll for r in res)
+    assert all(len(r[6]) == ncoll for r in res)  # one timing per real collective
+    tr = ExecutionTrace(world)
+    tr.records = [tuple(x) for x in recs]
+    assert tr.stages == ncoll * stage_count(world)
+    m, k = case["m"], case["k"]
+    carry_total = world * (world - 1) * m * k * 8
+    assert tr.total_bytes() >= carry_total
+    rep = audit_trace(tr, CostModelParams(1e-6, 1e-9, m, world), nrhs=k, collectives=ncoll)
+    assert rep["stages"] == tr.stages and rep["max_message_bytes"] <= (m * m + m) * 8 * k
+    x = np.concatenate([r[4] for r in res])
+    import blocktri_oracle as O
+
+    d, lo, up, f = configs.dominant_numpy(case["n"], m, k, seed=case["seed"])
+    assert O.max_rel_err(x, O.plan_solve(O.plan_build(d, lo, up, case["ranks"]), f)) <= 1e-9

@@ -101,7 +101,12 @@ def test_sharded_plan_over_nccl_world1():
         d, lo, up, f = configs.dominant_numpy(512, 16, 16, seed=9)
         plan = ShardedPlan(torch.from_numpy(d).cuda(), torch.from_numpy(lo).cuda(), torch.from_numpy(up).cuda(), 8,
                            split=2)
-        x = plan.solve(torch.from_numpy(f).cuda()).cpu().numpy()
+        from paper_1108_4181_b200.trace import ExecutionTrace
+
+        tr = ExecutionTrace(1)
+        x = plan.solve(torch.from_numpy(f).cuda(), trace=tr).cpu().numpy()
+        assert tr.stages == 0 and len(tr.timings) == plan.collectives_per_solve(16)  # NCCL timed by events
+        assert all(ms >= 0 for _label, ms in tr.timings)
         plan.close()
     finally:
         dist.destroy_process_group()
