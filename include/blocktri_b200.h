@@ -113,6 +113,18 @@ int btd_plan_export(btd_plan* plan, void* dst, int64_t* nbytes, void* stream);
 int btd_band_to_blocktri(const double* bands, int64_t n, int64_t d, int64_t m, double* diag, double* lower,
                          double* upper, void* stream);
 int btd_band_from_probes(const double* y, int64_t n, int64_t d, int64_t ldy, double* bands, void* stream);
+
+/* ---- operators around the path (Schur DD) -----------
+ * btd_blocktri_apply: y = P x with P block tridiagonal (ref core.py:118-127
+ *   BlockTriMatrix.apply; used by ref schur.py:191-195 BlocktriOperator.apply),
+ *   x, y (n, m, k) row-major on the device.
+ * btd_csr_spmm: y = alpha * S x + beta * y, S in CSR (int64 row pointers and
+ *   column indices), x (ncols, k), y (nrows, k) row-major on the device (the
+ *   interface couplings A_iG, A_iG^T, A_GG of ref schur.py:198-310). */
+int btd_blocktri_apply(const double* diag, const double* lower, const double* upper, int64_t n, int64_t m,
+                       const double* x, double* y, int64_t k, void* stream);
+int btd_csr_spmm(const int64_t* rowptr, const int64_t* col, const double* val, int64_t nrows, int64_t k,
+                 const double* x, double alpha, double beta, double* y, void* stream);
 int btd_plan_import(const void* src, int64_t nbytes, int device, void* stream, btd_plan** out_plan);
 
 /* ---- row-sharded (multi-GPU) plans and solves --------------------------

@@ -38,6 +38,8 @@ EXPORTS = (
     "btd_plan_import",
     "btd_band_to_blocktri",
     "btd_band_from_probes",
+    "btd_blocktri_apply",
+    "btd_csr_spmm",
     "btd_plan_create_shard",
     "btd_shard_contrib",
     "btd_shard_finish",
@@ -97,6 +99,10 @@ def load():
     lib.btd_band_to_blocktri.restype = i32
     lib.btd_band_from_probes.argtypes = [dp, i64, i64, i64, dp, vp]
     lib.btd_band_from_probes.restype = i32
+    lib.btd_blocktri_apply.argtypes = [dp, dp, dp, i64, i64, dp, dp, i64, vp]
+    lib.btd_blocktri_apply.restype = i32
+    lib.btd_csr_spmm.argtypes = [dp, dp, dp, i64, i64, dp, ctypes.c_double, ctypes.c_double, dp, vp]
+    lib.btd_csr_spmm.restype = i32
     lib.btd_plan_create_shard.argtypes = [dp, dp, dp, i64, i64, i64, i64, i32, i32, i32, i32, vp,
                                           ctypes.POINTER(vp), ctypes.POINTER(i64)]
     lib.btd_plan_create_shard.restype = i32

@@ -1634,6 +1634,39 @@ int btd_band_to_blocktri(const double* bands, int64_t n, int64_t d, int64_t m, d
   return BTD_OK;
 }
 
+int btd_blocktri_apply(const double* diag, const double* lower, const double* upper, int64_t n, int64_t m,
+                       const double* x, double* y, int64_t k, void* stream) {
+  g_err.clear();
+  if (n < 1 || m < 1 || k < 1) { g_err = "apply: need n, m, k >= 1"; return BTD_ERR_DIMENSION; }
+  if (!diag || !x || !y || (n > 1 && (!lower || !upper))) { g_err = "apply: NULL pointer"; return BTD_ERR_INVALID_ARG; }
+  try {
+    const int64_t total = n * m * k;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    blocktri_apply_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(diag, lower, upper, n, m, k, x, y);
+    CK_LAUNCH();
+  } catch (const BtdError& e) {
+    return e.code;
+  }
+  return BTD_OK;
+}
+
+int btd_csr_spmm(const int64_t* rowptr, const int64_t* col, const double* val, int64_t nrows, int64_t k,
+                 const double* x, double alpha, double beta, double* y, void* stream) {
+  g_err.clear();
+  if (nrows < 0 || k < 1) { g_err = "spmm: bad dimensions"; return BTD_ERR_DIMENSION; }
+  if (nrows == 0) return BTD_OK;
+  if (!rowptr || !y) { g_err = "spmm: NULL pointer"; return BTD_ERR_INVALID_ARG; }
+  try {
+    const int64_t total = nrows * k;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    csr_spmm_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(rowptr, col, val, nrows, k, x, alpha, beta, y);
+    CK_LAUNCH();
+  } catch (const BtdError& e) {
+    return e.code;
+  }
+  return BTD_OK;
+}
+
 int btd_band_from_probes(const double* y, int64_t n, int64_t d, int64_t ldy, double* bands, void* stream) {
   g_err.clear();
   if (n < 1 || d < 0) { g_err = "band: need n >= 1 and d >= 0"; return BTD_ERR_DIMENSION; }

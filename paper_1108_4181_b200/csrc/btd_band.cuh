@@ -58,3 +58,51 @@ __global__ void band_from_probes_kernel(const double* __restrict__ y, int64_t n,
 }
 
 }  // namespace btd
+
+namespace btd {
+
+// Operator application around the path (Schur DD, ref schur.py:168-195, core.py:118-127):
+// y_i = C_i x_i - A_i x_{i-1} - B_i x_{i+1}, blocks (n, m, m) / (n-1, m, m), x, y (n, m, k).
+// One thread per output entry; the three block rows it reads come from L1/L2.
+// Used for apply_full / residuals, not on the solve path.
+__global__ void blocktri_apply_kernel(const double* __restrict__ C, const double* __restrict__ A,
+                                      const double* __restrict__ B, int64_t n, int64_t m, int64_t k,
+                                      const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t total = n * m * k, mk = m * k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / mk, r = (e % mk) / k, c = e % k;
+    const double* cr = C + (i * m + r) * m;
+    const double* xi = x + i * mk + c;
+    double s = 0.0;
+    for (int64_t j = 0; j < m; ++j) s += cr[j] * xi[j * k];
+    if (i > 0) {
+      const double* ar = A + ((i - 1) * m + r) * m;
+      const double* xp = x + (i - 1) * mk + c;
+      for (int64_t j = 0; j < m; ++j) s -= ar[j] * xp[j * k];
+    }
+    if (i + 1 < n) {
+      const double* br = B + (i * m + r) * m;
+      const double* xn = x + (i + 1) * mk + c;
+      for (int64_t j = 0; j < m; ++j) s -= br[j] * xn[j * k];
+    }
+    y[e] = s;
+  }
+}
+
+// CSR sparse x dense (k columns, row-major): y = alpha * S x + beta * y.  Interface
+// couplings have a handful of entries per row; one thread per (row, column).
+__global__ void csr_spmm_kernel(const int64_t* __restrict__ rowptr, const int64_t* __restrict__ col,
+                                const double* __restrict__ val, int64_t nrows, int64_t k,
+                                const double* __restrict__ x, double alpha, double beta, double* __restrict__ y) {
+  const int64_t total = nrows * k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / k, c = e % k;
+    double s = 0.0;
+    for (int64_t p = rowptr[r]; p < rowptr[r + 1]; ++p) s += val[p] * x[col[p] * k + c];
+    y[e] = beta == 0.0 ? alpha * s : alpha * s + beta * y[e];
+  }
+}
+
+}  // namespace btd

@@ -54,6 +54,14 @@ class Breakdown(BlocktriError):
     """Conjugate-gradient breakdown (ref errors.py:56)."""
 
 
+class UnlabeledNode(BlocktriError):
+    """A mesh node is neither interior nor interface (ref errors.py:48)."""
+
+
+class SubdomainSolveFailure(BlocktriError):
+    """An interior solve inside the Schur complement failed (ref errors.py:52)."""
+
+
 class BandTooWide(BlocktriError):
     """Probing bandwidth does not fit the operator order (ref errors.py:60)."""
 
@@ -71,7 +79,7 @@ _BY_NAME = {
     c.__name__: c
     for c in (BlocktriError, DimensionMismatch, SingularBlock, SingularPivot,
               IndexOutOfRange, InvalidRankCount, InconsistentRanges, DeadlockDetected,
-              StageViolation, Breakdown, BandTooWide, BlockTooSmall, DeviceError)
+              StageViolation, Breakdown, UnlabeledNode, SubdomainSolveFailure, BandTooWide, BlockTooSmall, DeviceError)
 }
 
 

@@ -283,3 +283,9 @@ class HelmholtzDD:
         r[:, 1:] -= x[:, :-1]
         r[:, :-1] -= x[:, 1:]
         return float(r.abs().max() / f.abs().max())
+
+
+# The reference's generic matrix-free Schur API (ref schur.py:29-378), device-resident.
+from .schur_system import (INTERFACE_LABEL, BlocktriOperator, CgStats, SchurSystem, SubdomainBlock,  # noqa: E402
+                           cg_solve, gmres_solve, partition_numbering, probing_preconditioner,
+                           recover_interiors, schur_apply, schur_rhs, solve_interface, solve_schur)
