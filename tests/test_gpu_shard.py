@@ -18,7 +18,24 @@ from paper_1108_4181_b200.distributed import NativeBackend, ShardedPlan
 pytestmark = pytest.mark.gpu
 
 
-def _emulate(d, lo, up, f, ranks, split, world):
+def _reimport(h):
+    """export a finished shard plan image and import it as a fresh plan (row f2)."""
+    import ctypes
+
+    from paper_1108_4181_b200 import _native
+
+    lib = _native.load()
+    need = ctypes.c_int64(0)
+    assert lib.btd_plan_export(h, None, ctypes.byref(need), None) == 0
+    img = np.empty(need.value, np.uint8)
+    assert lib.btd_plan_export(h, ctypes.c_void_p(img.ctypes.data), ctypes.byref(need), None) == 0
+    out = ctypes.c_void_p()
+    assert lib.btd_plan_import(ctypes.c_void_p(img.ctypes.data), need.value, 0, None, ctypes.byref(out)) == 0
+    lib.btd_plan_destroy(h)
+    return out
+
+
+def _emulate(d, lo, up, f, ranks, split, world, reimport=False):
     import torch
 
     be = NativeBackend(0)
@@ -34,6 +51,8 @@ def _emulate(d, lo, up, f, ranks, split, world):
     for h in hs:
         st, row = be.finish(h, allc)
         assert st == 0
+    if reimport:
+        hs = [_reimport(h) for h in hs]
     infos = [be.info(h) for h in hs]
     k = f.shape[2]
     ft = torch.from_numpy(f).cuda()
@@ -74,6 +93,14 @@ def test_emulated_shards_match_oracle(world, n, m, k, ranks, split):
     ref = O.plan_solve(O.plan_build(d, lo, up, ranks), f)
     assert O.max_rel_err(res[1], ref) <= 1e-9
     assert O.rel_residual(d, lo, up, res[1], f) <= 1e-10
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_emulated_shard_plan_images(world):
+    d, lo, up, f = configs.dominant_numpy(203, 8, 5, seed=3)
+    a = _emulate(d, lo, up, f, 4, 2, world)
+    b = _emulate(d, lo, up, f, 4, 2, world, reimport=True)
+    assert a[0] == b[0] == "ok" and np.array_equal(a[1], b[1])
 
 
 def test_emulated_shard_singular_reports_first_range():
