@@ -48,8 +48,11 @@ sys.path.insert(0, ROOT)
 # reading of BASELINE.json: 8 / 16 / 32 / 64 subdomains per GPU on 1 / 2 / 4 / 8 GPUs.
 BENCH_CFG = {
     "c0": dict(subdomains_per_gpu=lambda w: 4, ranges_per_gpu=4),
-    "c1": dict(subdomains_per_gpu=lambda w: 18, ranges_per_gpu=18),
-    "c2": dict(subdomains_per_gpu=lambda w: 9, ranges_per_gpu=9),
+    # c1/c2: 36 ranges per GPU -- the device rate is flat in P (18..54 measured; the
+    # sweeps are DMMA-throughput-bound, not wave-quantised) while shorter chains cut the
+    # fill latency of the host pipeline (e2e +8.5% c1, +9% c2; profiles/r01_host_pipeline.txt)
+    "c1": dict(subdomains_per_gpu=lambda w: 36, ranges_per_gpu=36),
+    "c2": dict(subdomains_per_gpu=lambda w: 36, ranges_per_gpu=36),
     # c3: the explicit interface Schur complement S (N=63, M=2048) of the 64-subdomain
     # Helmholtz DD; P = 9 ranges of 7 interface rows on one GPU (288 GEMM tiles fill the
     # 296 CTA slots), P = 8 (a multiple of 2/4/8) when sharded
