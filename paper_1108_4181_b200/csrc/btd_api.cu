@@ -629,11 +629,14 @@ bool launch_stream(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
 void launch_chain(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
   if (a.nr <= 0) return;
   if (launch_stream(mp, a, fwd, st)) return;
-  static int variant = -1;
-  if (variant < 0) {
+  static int variant_f = -1, variant_b = -1;
+  if (variant_f < 0) {
     const char* e = getenv("BTD_CHAIN_VARIANT");
-    variant = e ? atoi(e) : 0;
+    variant_f = e ? atoi(e) : 0;
+    const char* eb = getenv("BTD_CHAIN_VARIANT_BWD");
+    variant_b = eb ? atoi(eb) : variant_f;
   }
+  const int variant = fwd ? variant_f : variant_b;
   switch (mp) {
     case 8: launch_chain_t<8, 32, 1, 4>(a, fwd, st); break;
     case 16: launch_chain_t<16, 16, 1, 1>(a, fwd, st); break;
@@ -642,12 +645,28 @@ void launch_chain(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
       if (variant == 2) launch_chain_t<64, 64, 8, 2, 2, 0>(a, fwd, st);
       else if (variant == 3) launch_chain_t<64, 64, 8, 2, 3, 0>(a, fwd, st);
       else if (variant == 4) launch_chain_t<64, 64, 8, 2, 2, 3>(a, fwd, st);
-      else launch_chain_t<64, 64, 8, 2>(a, fwd, st);
+      else if (variant == 5) launch_chain_t<64, 128, 8, 2, 2, 0>(a, fwd, st);
+      else if (variant == 6) launch_chain_t<64, 64, 4, 4>(a, fwd, st);
+      else if (variant == 7) launch_chain_t<64, 32, 8, 2>(a, fwd, st);
+      else if (variant == 8) launch_chain_t<64, 32, 8, 1>(a, fwd, st);
+      else if (variant == 9) launch_chain_t<64, 32, 4, 2>(a, fwd, st);
+      else if (variant == 10) launch_chain_t<64, 32, 8, 1, 2, 2>(a, fwd, st);
+      else if (variant == 11) launch_chain_t<64, 32, 8, 1, 4, 4>(a, fwd, st);
+      else if (variant == 12) launch_chain_t<64, 16, 8, 1>(a, fwd, st);
+      else if (variant == 13) launch_chain_t<64, 32, 8, 1, 3, 0>(a, fwd, st);
+      else if (variant == 14) launch_chain_t<64, 16, 4, 1>(a, fwd, st);
+      else if (fwd) launch_chain_t<64, 128, 8, 2, 2, 0>(a, fwd, st);  // measured best (c2): wide tiles forward,
+      else launch_chain_t<64, 32, 8, 1, 3, 0>(a, fwd, st);             // narrow register-prefetch tiles backward
       break;
     case 128: launch_chain_t<128, 32, 16, 1>(a, fwd, st); break;
     case 256:
       if (variant == 1) launch_chain_t<256, 32, 16, 1>(a, fwd, st);
-      else launch_chain_t<256, 16, 16, 1>(a, fwd, st);
+      else if (variant == 2) launch_chain_t<256, 16, 16, 1, 3, 0>(a, fwd, st);
+      else if (variant == 3) launch_chain_t<256, 8, 16, 1>(a, fwd, st);
+      else if (variant == 4) launch_chain_t<256, 16, 32, 1>(a, fwd, st);
+      else if (variant == 5) launch_chain_t<256, 32, 32, 1>(a, fwd, st);
+      else if (fwd) launch_chain_t<256, 16, 16, 1>(a, fwd, st);
+      else launch_chain_t<256, 32, 32, 1>(a, fwd, st);  // measured (c1): 32-warp CTAs backward, -4%
       break;
     default: fail(BTD_ERR_UNSUPPORTED, "no chain kernel for this block order");
   }

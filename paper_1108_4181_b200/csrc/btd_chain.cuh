@@ -238,6 +238,7 @@ struct ChainCfg {
   static constexpr int BWD_BUFS = 2 + NY;
   static_assert(RW % 8 == 0 && CW % 8 == 0, "warp tile must be a multiple of 8x8");
   static_assert(NS % PF == 0, "prefetch groups must tile a segment");
+  static_assert(NY != 1, "a one-deep y ring would read a tile before it is loaded");
 };
 
 // One prefetch group: PF pair steps of  acc += A_seg @ Bs, consuming the
