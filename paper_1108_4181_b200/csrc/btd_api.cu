@@ -34,6 +34,7 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
 #include <cusolverDn.h>
 
 #include "blocktri_b200.h"
@@ -238,6 +239,64 @@ struct SplitK {
   double* partial = nullptr;
 };
 
+// Tensor maps for the TMA-2D GEMM: each operand's backing array seen as a 2-D
+// [rows][ld] tensor (rows = index * stride / ld + row), 128-byte boxes, 128B swizzle.
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      fail(BTD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool encode_operand(CUtensorMap* map, const Opnd& o, int box_rows, int64_t* rpi) {
+  if (o.ld < 16 || o.stride % o.ld) return false;
+  *rpi = o.stride / o.ld;
+  const cuuint64_t dims[2] = {(cuuint64_t)o.ld, (cuuint64_t)1 << 30};
+  const cuuint64_t strides[1] = {(cuuint64_t)o.ld * 8};
+  const cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(o.base), dims,
+                                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool make_tma_operands(const GemmDesc& d, int bm, int bk, TmaOperands& ops) {
+  for (int i = 0; i < d.nterms; ++i) {
+    if (!encode_operand(&ops.a[i], d.t[i].A, bm, &ops.a_rpi[i])) return false;
+    if (!encode_operand(&ops.b[i], d.t[i].B, bk, &ops.b_rpi[i])) return false;
+    // int32 tensor coordinates: the rows any entry can reach stay below 2^30
+  }
+  return true;
+}
+
+// The warp-specialised TMA GEMM needs whole tiles, 32-multiple reductions, even
+// row strides and 16-byte aligned rows for every operand (bulk copies, double2 epilogue).
+bool ws_eligible(const GemmDesc& d, int bn) {
+  if (d.rows % 128 || d.cols % bn) return false;
+  auto ok = [](const Opnd& o) {
+    return o.base && !o.ld_arr && (o.ld % 2) == 0 && (o.stride % 2) == 0 &&
+           (reinterpret_cast<uintptr_t>(o.base) % 16) == 0;
+  };
+  for (int i = 0; i < d.nterms; ++i) {
+    const Term& t = d.t[i];
+    if (t.k_arr || t.k % 32 || !ok(t.A) || !ok(t.B)) return false;
+  }
+  if (d.split_b) {
+    if (d.kchunk % 32) return false;
+  } else if (!ok(d.C) || (d.Cin.base && !ok(d.Cin))) {
+    return false;
+  }
+  return true;
+}
+
 void launch_gemm(int64_t rows, int64_t cols, int nbatch, Opnd C, Opnd Cin, double beta,
                  std::initializer_list<Term> terms, cudaStream_t st, const SplitK* sp = nullptr) {
   if (nbatch <= 0 || rows <= 0 || cols <= 0) return;
@@ -260,7 +319,30 @@ void launch_gemm(int64_t rows, int64_t cols, int nbatch, Opnd C, Opnd Cin, doubl
   for (const Term& t : terms) d.t[d.nterms++] = t;
   const int gz = std::min(d.split_b ? d.nsplit_total : nbatch, 65535);
   auto tiles = [&](int64_t bm, int64_t bn) { return ((rows + bm - 1) / bm) * ((cols + bn - 1) / bn) * gz; };
-  if (rows >= 128 && cols >= 64 && tiles(128, 64) >= 148) {
+  static int ws_env = -1;
+  if (ws_env < 0) {
+    const char* e = getenv("BTD_GEMM_WS");
+    ws_env = e ? atoi(e) : 1;
+  }
+  TmaOperands ops;
+  if (ws_env == 1 && rows >= 128 && cols >= 64 && tiles(128, 64) >= 148 && ws_eligible(d, 64) &&
+      make_tma_operands(d, 128, 32, ops)) {
+    using C_ = TmaCfg<128, 64, 4, 2, 4>;
+    set_smem_attr((const void*)gemm_tma_kernel<128, 64, 4, 2, 4>, C_::SMEM);
+    dim3 grid((unsigned)(cols / 64), (unsigned)(rows / 128), gz);
+    gemm_tma_kernel<128, 64, 4, 2, 4><<<grid, C_::NT, C_::SMEM, st>>>(ops, d);
+  } else if (ws_env == 2 && rows >= 128 && cols >= 64 && tiles(128, 64) >= 148 && ws_eligible(d, 64)) {
+    using C_ = WsCfg<128, 64, 4, 2, 3>;
+    set_smem_attr((const void*)gemm_ws_kernel<128, 64, 4, 2, 3>, C_::SMEM);
+    dim3 grid((unsigned)(cols / 64), (unsigned)(rows / 128), gz);
+    gemm_ws_kernel<128, 64, 4, 2, 3><<<grid, C_::NT, C_::SMEM, st>>>(d);
+  } else if (ws_env == 3 && rows >= 128 && cols >= 128 && tiles(128, 128) >= 120 && ws_eligible(d, 128)) {
+    // one CTA per SM holds a 128 x 128 tile: 16 consumer warps of 32 x 32
+    using C_ = WsCfg<128, 128, 4, 4, 3>;
+    set_smem_attr((const void*)gemm_ws_kernel<128, 128, 4, 4, 3>, C_::SMEM);
+    dim3 grid((unsigned)(cols / 128), (unsigned)(rows / 128), gz);
+    gemm_ws_kernel<128, 128, 4, 4, 3><<<grid, C_::NT, C_::SMEM, st>>>(d);
+  } else if (rows >= 128 && cols >= 64 && tiles(128, 64) >= 148) {
     using C_ = PipeCfg<128, 64, 4, 2, 3>;
     set_smem_attr((const void*)gemm_pipe_kernel<128, 64, 4, 2, 3>, C_::SMEM);
     dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 127) / 128), gz);
