@@ -121,7 +121,7 @@ __global__ void set_identity_kernel(double* dst, int mp) {
 }
 
 // R_node[a][i*mp + c] = Y_i[c][a]  (ref dichotomy.py:145: y.transpose(2,0,1))
-__global__ void assemble_rows_kernel(const double* Y, const int64_t* ynb0, const int64_t* roff,
+__global__ void assemble_rows_kernel(const double* Y, const int64_t* ynb0, const int64_t* roff, const int64_t* ld,
                                      const int64_t* size, const int64_t* eoff, int nnodes,
                                      int64_t total, int mp, double* R) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -136,7 +136,7 @@ __global__ void assemble_rows_kernel(const double* Y, const int64_t* ynb0, const
     const int64_t s = size[b];
     const int64_t a = le / (s * mp), rest = le % (s * mp);
     const int64_t i = rest / mp, c = rest % mp;
-    R[roff[b] + a * s * mp + i * mp + c] = Y[(ynb0[b] + i) * (int64_t)mp * mp + c * mp + a];
+    R[roff[b] + a * ld[b] + i * mp + c] = Y[(ynb0[b] + i) * (int64_t)mp * mp + c * mp + a];
   }
 }
 
@@ -287,7 +287,8 @@ bool ws_eligible(const GemmDesc& d, int bn) {
   };
   for (int i = 0; i < d.nterms; ++i) {
     const Term& t = d.t[i];
-    if (t.k_arr || t.k % 32 || !ok(t.A) || !ok(t.B)) return false;
+    // with k_arr, t.k is a divisor of every per-entry reduction length (its granularity)
+    if (t.k <= 0 || t.k % 32 || !ok(t.A) || !ok(t.B)) return false;
   }
   if (d.split_b) {
     if (d.kchunk % 32) return false;
@@ -424,6 +425,9 @@ struct btd_plan {
   const int64_t *z_id = nullptr, *z_roff = nullptr, *z_rld = nullptr, *z_nlo = nullptr;
   SplitK z_split;
   std::vector<int64_t> z_k;  // reduction length per z entry (host)
+  const int64_t* z_kd = nullptr;  // ... (device)
+  bool r_uniform = false;         // inverse rows stored with the common stride r_ld
+  int64_t r_ld = 0;
   struct Level {
     int count = 0;
     const int64_t *c_idx = nullptr, *z_idx = nullptr, *e_idx = nullptr, *xl_idx = nullptr,
@@ -1030,13 +1034,13 @@ SplitK make_split(btd_plan& pl, const std::vector<int64_t>& kper, int64_t tiles_
   for (int64_t k : kper) { base += tiles_per_entry; kmax = std::max(kmax, k); }
   if (kper.empty() || base >= want * 2) return sp;
   // chunk: the largest multiple of 16 that still yields >= want CTAs in total (and >= 64 long)
-  int64_t chunk = std::max<int64_t>(64, (kmax + 15) / 16 * 16);
+  int64_t chunk = std::max<int64_t>(64, (kmax + 31) / 32 * 32);
   auto total = [&](int64_t ch) {
     int64_t t = 0;
     for (int64_t k : kper) t += (k + ch - 1) / ch;
     return t;
   };
-  while (chunk > 64 && total(chunk) * tiles_per_entry < want) chunk = std::max<int64_t>(64, (chunk / 2 + 15) / 16 * 16);
+  while (chunk > 64 && total(chunk) * tiles_per_entry < want) chunk = std::max<int64_t>(64, (chunk / 2 + 31) / 32 * 32);
   const int64_t nt = total(chunk);
   if (nt <= (int64_t)kper.size()) return sp;  // no entry split: plain launch
   std::vector<int32_t> sb, sk, zoff, zcnt;
@@ -1110,17 +1114,25 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
   std::vector<int64_t> nb0(nn), sz(nn), roff(nn), rld(nn), eoff(nn + 1);
   int64_t tot = 0, rtot = 0;
   int64_t maxlevel = 0;
+  // Large blocks store every node's rows with one common row stride (the widest
+  // node), so the series-sum GEMM sees a plain strided operand (TMA tensor map).
+  pl.r_uniform = mp >= 128;
+  int64_t maxsz = 0;
+  for (int b = 0; b < nn; ++b) maxsz = std::max<int64_t>(maxsz, pl.nodes[b].hi - pl.nodes[b].lo + 1);
+  pl.r_ld = maxsz * mp;
+  int64_t ecount = 0;
   for (int b = 0; b < nn; ++b) {
     sz[b] = pl.nodes[b].hi - pl.nodes[b].lo + 1;
     nb0[b] = tot;
     tot += sz[b];
-    roff[b] = rtot;
-    rld[b] = sz[b] * mp;
-    eoff[b] = rtot;
-    rtot += sz[b] * blk;
+    rld[b] = pl.r_uniform ? pl.r_ld : sz[b] * mp;
+    roff[b] = pl.r_uniform ? (int64_t)b * mp * pl.r_ld : rtot;
+    eoff[b] = ecount;
+    ecount += sz[b] * blk;
+    rtot = pl.r_uniform ? (int64_t)(b + 1) * mp * pl.r_ld : rtot + sz[b] * blk;
     maxlevel = std::max(maxlevel, pl.nodes[b].level);
   }
-  eoff[nn] = rtot;
+  eoff[nn] = ecount;
   DevBuf tp, tfs, tfc, ws;
   double* T = nullptr;
   const int64_t tpY = 3 * tot;
@@ -1218,8 +1230,9 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
   if (!restore) {
     std::vector<int64_t> ynb0(nn);
     for (int b = 0; b < nn; ++b) ynb0[b] = tpY + nb0[b];
-    assemble_rows_kernel<<<1184, 256, 0, st>>>(T, pl.upload(ynb0), pl.upload(roff), pl.upload(sz), pl.upload(eoff), nn,
-                                              rtot, (int)mp, pl.Rrows.d());
+    if (pl.r_uniform) CK(cudaMemsetAsync(pl.Rrows.p, 0, (size_t)rtot * sizeof(double), st));
+    assemble_rows_kernel<<<1184, 256, 0, st>>>(T, pl.upload(ynb0), pl.upload(roff), pl.upload(rld), pl.upload(sz),
+                                              pl.upload(eoff), nn, ecount, (int)mp, pl.Rrows.d());
     CK_LAUNCH();
   }
   pl.d_roff = pl.upload(roff);
@@ -1317,7 +1330,10 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
       L_.e_k = pl.upload(ek); L_.h_k = pl.upload(hk);
     }
     // split-K plans: enough CTAs (>= 2 waves) for the series sums and the level corrections
-    pl.z_k = zrl;
+    pl.z_k.clear();
+    for (int b = 0; b < nn; ++b)
+      if (need_k[pl.nodes[b].k] && !crossing[b]) pl.z_k.push_back(sz[b] * mp);
+    pl.z_kd = pl.upload(pl.z_k);
     build_splits(pl);
     // fused cooperative tree for small blocks on a single rank
     const char* ft_env = getenv("BTD_FUSED_TREE");
@@ -1432,6 +1448,15 @@ void solve_forward(btd_plan& pl, const double* F, double* X, int64_t K, double* 
   }
 }
 
+// z_node = R_node f~[lo..hi] for the needed nodes: reduction length size * mp per node
+Term z_term(btd_plan& pl, double* ft, int64_t K) {
+  const int64_t mpK = pl.mp * K;
+  if (pl.r_uniform)  // node rows at b * mp * r_ld with stride r_ld: a plain strided operand
+    return term(mk(pl.Rrows.d(), pl.z_id, 0, pl.mp * pl.r_ld, pl.r_ld), mk(ft, pl.z_nlo, 0, mpK, K), pl.mp, 1.0,
+                pl.z_kd);
+  return term(mk(pl.Rrows.d(), pl.z_roff, 0, 1, 0, pl.z_rld), mk(ft, pl.z_nlo, 0, mpK, K), 0, 1.0, pl.z_kd);
+}
+
 // split-K maps with the current scratch slot's partial buffer
 const SplitK* split_with(const SplitK& sp, btd_plan& pl) {
   static thread_local SplitK tmp;
@@ -1484,9 +1509,7 @@ void solve_tree(btd_plan& pl, int64_t K, cudaStream_t st) {
       default: break;
     }
   }
-  launch_gemm(mp, K, pl.nz, mk(pl.S().zbuf.d(), pl.z_id, 0, mpK, K), none(), 0.0,
-              {term(mk(pl.Rrows.d(), pl.z_roff, 0, 1, 0, pl.z_rld), mk(pl.S().ft.d(), pl.z_nlo, 0, mpK, K), 0, 1.0,
-                    pl.z_rld)},
+  launch_gemm(mp, K, pl.nz, mk(pl.S().zbuf.d(), pl.z_id, 0, mpK, K), none(), 0.0, {z_term(pl, pl.S().ft.d(), K)},
               st, split_with(pl.z_split, pl));
   solve_levels(pl, K, st);
 }
@@ -1633,7 +1656,7 @@ void solve_shard_b(btd_plan& pl, const double* carry_all, double* partial_out, i
     CK_LAUNCH();
   }
   launch_gemm(mp, K, pl.nz, mk(pl.S().zbuf.d(), pl.z_id, 0, mpK, K), none(), 0.0,
-              {term(mk(pl.Rrows.d(), pl.z_roff, 0, 1, 0, pl.z_rld), mk(ft, pl.z_nlo, 0, mpK, K), 0, 1.0, pl.z_rld)}, st,
+              {z_term(pl, ft, K)}, st,
               split_with(pl.z_split, pl));
   launch_gemm(mp, K, pl.ncross, mk(partial_out, nullptr, 0, mpK, K), none(), 0.0,
               {term(mk(pl.Rrows.d(), pl.cross_roff, 0, 1, 0, pl.cross_ld), mk(ft, pl.cross_lo, 0, mpK, K), 0, 1.0,

@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(32 * (WGM * WGN + 1), 1) gemm_ws_kernel(GemmDe
         const double* A = opnd_ptr(tm_.A, b);
         const double* B = opnd_ptr(tm_.B, b);
         const int64_t lda = tm_.A.ld, ldb = tm_.B.ld;
-        int64_t K = tm_.k;
+        int64_t K = tm_.k_arr ? tm_.k_arr[b] : tm_.k;
         if (d.split_b) {
           const int64_t k0 = (int64_t)d.split_k[zz] * d.kchunk;
           A += k0;
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(32 * (WGM * WGN + 1), 1) gemm_ws_kernel(GemmDe
       for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     for (int ti = 0; ti < d.nterms; ++ti) {
       const Term& tm_ = d.t[ti];
-      int64_t K = tm_.k;
+      int64_t K = tm_.k_arr ? tm_.k_arr[b] : tm_.k;
       if (d.split_b) {
         const int64_t k0 = (int64_t)d.split_k[zz] * d.kchunk;
         K = K - k0 < d.kchunk ? K - k0 : d.kchunk;
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(32 * (WGM * WGN + 1), 1)
           const Term& tm_ = d.t[ti];
           const int64_t ai = (tm_.A.idx ? tm_.A.idx[b] : (int64_t)b) + tm_.A.add;
           const int64_t bi = (tm_.B.idx ? tm_.B.idx[b] : (int64_t)b) + tm_.B.add;
-          int64_t K = tm_.k, k0 = 0;
+          int64_t K = tm_.k_arr ? tm_.k_arr[b] : tm_.k, k0 = 0;
           if (d.split_b) {
             k0 = (int64_t)d.split_k[zz] * d.kchunk;
             K = K - k0 < d.kchunk ? K - k0 : d.kchunk;
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(32 * (WGM * WGN + 1), 1)
       for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     for (int ti = 0; ti < d.nterms; ++ti) {
       const Term& tm_ = d.t[ti];
-      int64_t K = tm_.k;
+      int64_t K = tm_.k_arr ? tm_.k_arr[b] : tm_.k;
       if (d.split_b) {
         const int64_t k0 = (int64_t)d.split_k[zz] * d.kchunk;
         K = K - k0 < d.kchunk ? K - k0 : d.kchunk;

@@ -194,3 +194,20 @@ def test_full_schur_dd_pipeline_matches_monolithic(nx, nz, nsub, groups):
     ref = spl.spsolve(schur.grid_operator(nx, nz).tocsc(), f.reshape(nz * nx, 3)).reshape(nz, nx, 3)
     assert np.abs(x - ref).max() <= 1e-9 * np.abs(ref).max()
     assert dd.residual(torch.from_numpy(x).cuda(), torch.from_numpy(f).cuda()) <= 1e-10
+
+
+@pytest.mark.parametrize("n,m,k,ranks,split,mode", [
+    (40, 256, 64, 8, 1, "0"),    # uniform-stride inverse rows + TMA series-sum GEMM (mp >= 128)
+    (30, 384, 128, 6, 1, "1"),   # mode 1: per-step sweep products on the TMA GEMM (rows % 128 == 0)
+    (21, 512, 64, 7, 1, "1"),    # cuSOLVER inverses (mp > 256) + TMA GEMM
+    (50, 128, 192, 10, 2, "0"),  # split second level, 3 column tiles
+])
+def test_large_blocks_tma_gemm_paths(n, m, k, ranks, split, mode, monkeypatch):
+    monkeypatch.setenv("BTD_FORCE_MODE", mode)
+    d, lo, up, f = configs.dominant_numpy(n, m, k, seed=m + n)
+    plan = plan_build(BlockTriMatrix(d, lo, up), ranks, split=split)
+    import torch
+
+    x = plan_solve(plan, torch.from_numpy(f).cuda()).cpu().numpy()
+    ref = O.plan_solve(O.plan_build(d, lo, up, ranks), f)
+    _check(d, lo, up, x, f, ref)
