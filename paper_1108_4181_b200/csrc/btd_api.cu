@@ -1921,7 +1921,12 @@ int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int6
     }
     // measured (profiles/r01_host_pipeline.txt): 32-column chunks of a 256-column
     // solve lose more to per-chunk solve latency than they gain in fill time
-    const int64_t minw = k >= 256 ? 64 : 32;
+    static int64_t minw_env = -1;
+    if (minw_env < 0) {
+      const char* e = getenv("BTD_HOST_MINW");
+      minw_env = e ? std::max(2, atoi(e)) : 0;
+    }
+    const int64_t minw = minw_env ? minw_env : (k >= 256 ? 64 : 32);
     int64_t kc = k;
     for (int64_t nch = maxch; nch >= 2; --nch)
       if (k % nch == 0 && (k / nch) % 2 == 0 && k / nch >= minw) { kc = k / nch; break; }
