@@ -19,7 +19,8 @@ for arg in sys.argv[2:]:
         # only this library's kernels (the bench also runs cuBLAS / torch kernels)
         if len(r) > vi and r[mi] == "gpu__time_duration.sum" and "btd::" in r[ki]:
             v = float(r[vi].replace(",", ""))
-            v = v / 1000.0 if r[ui] == "nsecond" else (v * 1000.0 if r[ui] == "msecond" else v)
+            u = r[ui]
+            v = v / 1000.0 if u in ("ns", "nsecond") else (v * 1000.0 if u in ("ms", "msecond") else v)
             t.append((r[ki].split("(")[0][:60], v))
     step = t[-n:]
     tot = sum(v for _, v in step)
