@@ -744,7 +744,15 @@ void launch_chain(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
       else if (fwd) launch_chain_t<64, 128, 8, 2, 2, 0>(a, fwd, st);  // measured best (c2): wide tiles forward,
       else launch_chain_t<64, 32, 8, 1, 3, 0>(a, fwd, st);             // narrow register-prefetch tiles backward
       break;
-    case 128: launch_chain_t<128, 32, 16, 1>(a, fwd, st); break;
+    case 128:
+      if (variant == 1) launch_chain_t<128, 64, 16, 2>(a, fwd, st);
+      else if (variant == 2) launch_chain_t<128, 64, 16, 1>(a, fwd, st);
+      else if (variant == 3) launch_chain_t<128, 16, 16, 1>(a, fwd, st);
+      else if (variant == 4) launch_chain_t<128, 32, 8, 1>(a, fwd, st);
+      else if (variant == 5) launch_chain_t<128, 32, 16, 2>(a, fwd, st);
+      else if (variant == 6) launch_chain_t<128, 32, 16, 1>(a, fwd, st);
+      else launch_chain_t<128, 64, 16, 1>(a, fwd, st);  // measured best on the c3dd interiors (+7%)
+      break;
     case 256:
       if (variant == 1) launch_chain_t<256, 32, 16, 1>(a, fwd, st);
       else if (variant == 2) launch_chain_t<256, 16, 16, 1, 3, 0>(a, fwd, st);
@@ -1116,10 +1124,14 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
   int64_t maxlevel = 0;
   // Large blocks store every node's rows with one common row stride (the widest
   // node), so the series-sum GEMM sees a plain strided operand (TMA tensor map).
-  pl.r_uniform = mp >= 128;
-  int64_t maxsz = 0;
-  for (int b = 0; b < nn; ++b) maxsz = std::max<int64_t>(maxsz, pl.nodes[b].hi - pl.nodes[b].lo + 1);
+  // (only while the padding costs at most 2 GB: deep trees keep the compact layout)
+  int64_t maxsz = 0, sumsz = 0;
+  for (int b = 0; b < nn; ++b) {
+    maxsz = std::max<int64_t>(maxsz, pl.nodes[b].hi - pl.nodes[b].lo + 1);
+    sumsz += pl.nodes[b].hi - pl.nodes[b].lo + 1;
+  }
   pl.r_ld = maxsz * mp;
+  pl.r_uniform = mp >= 128 && ((int64_t)nn * maxsz - sumsz) * blk * (int64_t)sizeof(double) <= (int64_t(2) << 30);
   int64_t ecount = 0;
   for (int b = 0; b < nn; ++b) {
     sz[b] = pl.nodes[b].hi - pl.nodes[b].lo + 1;
