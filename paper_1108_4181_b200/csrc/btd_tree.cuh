@@ -74,6 +74,41 @@ BTD_DEVINL void gmem_mma(double (&acc)[TM][TN][2], const double* __restrict__ A,
   }
 }
 
+// One block's fragments for gmem_mma (A: MP x MP at lda; B: MP x 16 cols from col0),
+// loaded ahead of use so a chunk's block products overlap their global loads.
+template <int MP, int TM, int TN>
+struct BlkFrag {
+  double2 a[MP / 8][TM];
+  double b0[MP / 8][TN], b1[MP / 8][TN];
+  BTD_DEVINL void load(const double* __restrict__ A, int64_t lda, const double* __restrict__ B, int64_t ldb,
+                       int64_t col0, int64_t K, int g, int t) {
+#pragma unroll
+    for (int s = 0; s < MP / 8; ++s) {
+#pragma unroll
+      for (int i = 0; i < TM; ++i) a[s][i] = ldg_cg2(A + (int64_t)(i * 8 + g) * lda + 8 * s + 2 * t);
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const bool in = col0 + j * 8 + g < K;
+        b0[s][j] = in ? __ldcg(B + (int64_t)(8 * s + 2 * t) * ldb + j * 8 + g) : 0.0;
+        b1[s][j] = in ? __ldcg(B + (int64_t)(8 * s + 2 * t + 1) * ldb + j * 8 + g) : 0.0;
+      }
+    }
+  }
+  BTD_DEVINL void mma(double (&acc)[TM][TN][2]) const {
+#pragma unroll
+    for (int s = 0; s < MP / 8; ++s) {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[s][i].x, b0[s][j]);
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[s][i].y, b1[s][j]);
+    }
+  }
+};
+
 template <int TM, int TN>
 BTD_DEVINL void acc_add_tile(double (&acc)[TM][TN][2], const double* __restrict__ P, int64_t K, int64_t col0, int g,
                              int t) {
@@ -85,6 +120,21 @@ BTD_DEVINL void acc_add_tile(double (&acc)[TM][TN][2], const double* __restrict_
       const double* p = P + (int64_t)(i * 8 + g) * K + c;
       if (c < K) acc[i][j][0] += __ldcg(p);
       if (c + 1 < K) acc[i][j][1] += __ldcg(p + 1);
+    }
+}
+
+// v = P tile (zeros outside the K columns), the loads acc_add_tile would issue
+template <int TM, int TN>
+BTD_DEVINL void acc_load_tile(double (&v)[TM][TN][2], const double* __restrict__ P, int64_t K, int64_t col0, int g,
+                              int t) {
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t c = col0 + j * 8 + 2 * t;
+      const double* p = P + (int64_t)(i * 8 + g) * K + c;
+      v[i][j][0] = c < K ? __ldcg(p) : 0.0;
+      v[i][j][1] = c + 1 < K ? __ldcg(p + 1) : 0.0;
     }
 }
 
@@ -125,10 +175,27 @@ __global__ void __launch_bounds__(256) tree_small_kernel(TreeArgs a) {
 #pragma unroll
       for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     const int64_t ld = a.rld[b];
-    for (int e = 0; e < a.ch_nblk[c]; ++e) {
-      const int64_t bk = a.ch_blk0[c] + e;
-      gmem_mma<MP, TM, TN>(acc, a.R + a.roff[b] + bk * MP, ld, a.ft + (a.lo[b] + bk) * mpK + col0, K, col0, K, g, t);
+    const int nblk = a.ch_nblk[c];
+    const int64_t bk0 = a.ch_blk0[c];
+    const double* Rb = a.R + a.roff[b];
+    const double* Fb = a.ft + a.lo[b] * mpK + col0;
+    if constexpr (MP >= 32) {  // two fragment sets would not fit the register budget
+      for (int e = 0; e < nblk; ++e)
+        gmem_mma<MP, TM, TN>(acc, Rb + (bk0 + e) * MP, ld, Fb + (bk0 + e) * mpK, K, col0, K, g, t);
+      acc_store_tile(acc, a.partial + (int64_t)c * mpK, K, col0, g, t);
+      continue;
     }
+    // block e+1's fragments are in flight while block e's products run (same order of sums)
+    BlkFrag<MP, TM, TN> fa, fb;
+    fa.load(Rb + bk0 * MP, ld, Fb + bk0 * mpK, K, col0, K, g, t);
+    int e = 0;
+    for (; e + 1 < nblk; e += 2) {
+      fb.load(Rb + (bk0 + e + 1) * MP, ld, Fb + (bk0 + e + 1) * mpK, K, col0, K, g, t);
+      fa.mma(acc);
+      if (e + 2 < nblk) fa.load(Rb + (bk0 + e + 2) * MP, ld, Fb + (bk0 + e + 2) * mpK, K, col0, K, g, t);
+      fb.mma(acc);
+    }
+    if (e < nblk) fa.mma(acc);
     acc_store_tile(acc, a.partial + (int64_t)c * mpK, K, col0, g, t);
   }
   grid.sync();
@@ -143,7 +210,27 @@ __global__ void __launch_bounds__(256) tree_small_kernel(TreeArgs a) {
       for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-      for (int c = 0; c < a.zc_cnt[b]; ++c) acc_add_tile(acc, a.partial + (int64_t)(a.zc_off[b] + c) * mpK, K, col0, g, t);
+      {  // partial sums in chunk order, loads U chunks ahead
+        const double* P0 = a.partial + (int64_t)a.zc_off[b] * mpK;
+        const int ncnt = a.zc_cnt[b];
+        int c = 0;
+        constexpr int U = MP <= 16 ? 4 : 2;  // loads in flight (register budget)
+        for (; c + U <= ncnt; c += U) {
+          double v[U][TM][TN][2];
+#pragma unroll
+          for (int u = 0; u < U; ++u) acc_load_tile(v[u], P0 + (int64_t)(c + u) * mpK, K, col0, g, t);
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+              for (int j = 0; j < TN; ++j) {
+                acc[i][j][0] += v[u][i][j][0];
+                acc[i][j][1] += v[u][i][j][1];
+              }
+        }
+        for (; c < ncnt; ++c) acc_add_tile(acc, P0 + (int64_t)c * mpK, K, col0, g, t);
+      }
       if (a.has_e[b])
         gmem_mma<MP, TM, TN>(acc, a.EH + (2 * (int64_t)b) * blk, MP, a.xt + a.xl[b] * mpK + col0, K, col0, K, g, t);
       if (a.has_h[b])
