@@ -48,11 +48,12 @@ sys.path.insert(0, ROOT)
 # reading of BASELINE.json: 8 / 16 / 32 / 64 subdomains per GPU on 1 / 2 / 4 / 8 GPUs.
 BENCH_CFG = {
     "c0": dict(subdomains_per_gpu=lambda w: 4, ranges_per_gpu=4),
-    # c1/c2: 36 ranges per GPU -- the device rate is flat in P (18..54 measured; the
-    # sweeps are DMMA-throughput-bound, not wave-quantised) while shorter chains cut the
-    # fill latency of the host pipeline (e2e +8.5% c1, +9% c2; profiles/r01_host_pipeline.txt)
-    "c1": dict(subdomains_per_gpu=lambda w: 36, ranges_per_gpu=36),
-    "c2": dict(subdomains_per_gpu=lambda w: 36, ranges_per_gpu=36),
+    # c1/c2: 37 ranges per GPU (148 = 4 x 37): every chain kernel's grid is a whole number
+    # of waves (c1 fwd 37 x 16 tiles = 4 x 148 CTAs, bwd 37 x 8 = 2 x 148; c2 fwd 37 x 8 =
+    # 2 x 148).  Measured on B200 (profiles/r01_ranks_sweep.txt): c1 P=36 0.848 -> P=37 0.868
+    # of roofline, c2 0.785 -> 0.802; P=48 or 56 drops to 0.69-0.75 (partial last wave)
+    "c1": dict(subdomains_per_gpu=lambda w: 37, ranges_per_gpu=37),
+    "c2": dict(subdomains_per_gpu=lambda w: 37, ranges_per_gpu=37),
     # c3: the explicit interface Schur complement S (N=63, M=2048) of the 64-subdomain
     # Helmholtz DD; P = 9 ranges of 7 interface rows on one GPU (288 GEMM tiles fill the
     # 296 CTA slots), P = 8 (a multiple of 2/4/8) when sharded
@@ -86,18 +87,40 @@ def log(*a):
 
 # --------------------------------------------------------------------------- helpers
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML polled
+    every 5 ms from a thread (short timed regions still get samples), else
+    ``nvidia-smi -lms 100``."""
 
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, period_s=0.005):
         self.index = index
+        self.period = period_s
         self.proc = None
+        self.nvml = None
         self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons)
+        self._stop = threading.Event()
 
     def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self._physical_index())
+            self.bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                         "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                         "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                         "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:  # no NVML: nvidia-smi
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -108,11 +131,33 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _physical_index(self):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [v.strip() for v in vis.split(",") if v.strip()]
+        if ids and self.index < len(ids) and ids[self.index].isdigit():
+            return int(ids[self.index])
+        return self.index
+
+    def _poll(self):
+        nv = self.nvml
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((float(sm), float(mx), {k for k, b in self.bits.items() if r & b}))
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self._stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=2)
         if self.proc:
             self.proc.terminate()
             try:
@@ -121,22 +166,22 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        samples = list(self.samples)
         for ln in self.lines:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 7:
                 continue
             try:
-                sm.append(float(p[0]))
-                mx = max(mx, float(p[1]))
+                samples.append((float(p[0]), float(p[1]),
+                                {nm for nm, v in zip(self.NAMES, p[3:7]) if v.lower().startswith("active")}))
             except ValueError:
                 continue
-            for nm, v in zip(names, p[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
+        sm = [x[0] for x in samples]
+        mx = max((x[1] for x in samples), default=0.0)
+        reasons = set().union(*[x[2] for x in samples]) if samples else set()
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml 5 ms" if self.nvml is not None else "nvidia-smi 100 ms"}
 
 
 def measured_peaks():

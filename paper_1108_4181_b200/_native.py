@@ -14,7 +14,8 @@ import os
 from . import errors as _err
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libblocktri_b200.so")
+# BTD_LIB_PATH: an alternative in-tree build of the same library (A/B tuning runs)
+LIB_PATH = os.environ.get("BTD_LIB_PATH") or os.path.join(LIB_DIR, "libblocktri_b200.so")
 
 BTD_OK = 0
 BTD_ERR_DIMENSION = 1

@@ -40,22 +40,27 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in _sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
+    """Build the library into ``out`` (``defines``: extra -D flags, for A/B variants)."""
+    if not force and out == OUT and up_to_date():
         return OUT
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp",
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp",
            os.path.join(CSRC, "btd_api.cu"), "-lcusolver", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr[-4000:]}")
-    os.replace(OUT + ".tmp", OUT)
+    os.replace(out + ".tmp", out)
     if verbose:
         sys.stderr.write(res.stderr)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python -m paper_1108_4181_b200.build [--force] [-v] [--out PATH] [-DNAME=V ...]
+    argv = sys.argv[1:]
+    out = argv[argv.index("--out") + 1] if "--out" in argv else OUT
+    defs = [a[2:] for a in argv if a.startswith("-D")]
+    print(build(force="--force" in argv, verbose="-v" in argv, out=out, defines=defs))

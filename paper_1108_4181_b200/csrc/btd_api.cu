@@ -741,6 +741,10 @@ void launch_chain(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
       else if (variant == 12) launch_chain_t<64, 16, 8, 1>(a, fwd, st);
       else if (variant == 13) launch_chain_t<64, 32, 8, 1, 3, 0>(a, fwd, st);
       else if (variant == 14) launch_chain_t<64, 16, 4, 1>(a, fwd, st);
+      else if (variant == 15) launch_chain_t<64, 128, 4, 4, 2, 0>(a, fwd, st);
+      else if (variant == 16) launch_chain_t<64, 128, 8, 4, 2, 0>(a, fwd, st);
+      else if (variant == 17) launch_chain_t<64, 64, 8, 2, 2, 0>(a, fwd, st);
+      else if (variant == 18) launch_chain_t<64, 64, 4, 2, 2, 0>(a, fwd, st);
       else if (fwd) launch_chain_t<64, 128, 8, 2, 2, 0>(a, fwd, st);  // measured best (c2): wide tiles forward,
       else launch_chain_t<64, 32, 8, 1, 3, 0>(a, fwd, st);             // narrow register-prefetch tiles backward
       break;
@@ -759,6 +763,10 @@ void launch_chain(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
       else if (variant == 3) launch_chain_t<256, 8, 16, 1>(a, fwd, st);
       else if (variant == 4) launch_chain_t<256, 16, 32, 1>(a, fwd, st);
       else if (variant == 5) launch_chain_t<256, 32, 32, 1>(a, fwd, st);
+      else if (variant == 6) launch_chain_t<256, 32, 8, 2>(a, fwd, st);
+      else if (variant == 7) launch_chain_t<256, 32, 16, 2>(a, fwd, st);
+      else if (variant == 8) launch_chain_t<256, 64, 16, 2>(a, fwd, st);
+      else if (variant == 9) launch_chain_t<256, 16, 16, 2>(a, fwd, st);
       else if (fwd) launch_chain_t<256, 16, 16, 1>(a, fwd, st);
       else launch_chain_t<256, 32, 32, 1>(a, fwd, st);  // measured (c1): 32-warp CTAs backward, -4%
       break;

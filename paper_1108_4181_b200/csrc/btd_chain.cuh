@@ -70,13 +70,8 @@ BTD_DEVINL void wgemm(double (&acc)[TM][TN][2], const double* __restrict__ A,
         b0[j] = Bs[(8 * s + 2 * t) * ldb + j * 8 + g];
         b1[j] = Bs[(8 * s + 2 * t + 1) * ldb + j * 8 + g];
       }
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) {
-          dmma(acc[i][j][0], acc[i][j][1], a[i].x, b0[j]);
-          dmma(acc[i][j][0], acc[i][j][1], a[i].y, b1[j]);
-        }
+      mma_k4<TM, TN, false>(acc, a, b0);
+      mma_k4<TM, TN, true>(acc, a, b1);
     }
   }
 }
@@ -117,15 +112,10 @@ BTD_DEVINL void wgemm2(double (&acc1)[TM][TN][2], const double* __restrict__ A1,
         b0[j] = Bs[(8 * s + 2 * t) * ldb + j * 8 + g];
         b1[j] = Bs[(8 * s + 2 * t + 1) * ldb + j * 8 + g];
       }
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) {
-          dmma(acc1[i][j][0], acc1[i][j][1], a1[i].x, b0[j]);
-          dmma(acc1[i][j][0], acc1[i][j][1], a1[i].y, b1[j]);
-          dmma(acc2[i][j][0], acc2[i][j][1], a2[i].x, b0[j]);
-          dmma(acc2[i][j][0], acc2[i][j][1], a2[i].y, b1[j]);
-        }
+      mma_k4<TM, TN, false>(acc1, a1, b0);
+      mma_k4<TM, TN, false>(acc2, a2, b0);
+      mma_k4<TM, TN, true>(acc1, a1, b1);
+      mma_k4<TM, TN, true>(acc2, a2, b1);
     }
   }
 }
@@ -217,6 +207,39 @@ BTD_DEVINL void cp_tile(double* Ys, const double* __restrict__ P, int64_t K, int
   cp_async_commit();
 }
 
+// Column-group variant of cp_tile: the NTG threads of one warp-column group copy
+// columns [c0, c0 + W) into dst (already offset to the group's first column).
+template <int W, int LD, int NTG>
+BTD_DEVINL void cp_tile_cols(double* dst, const double* __restrict__ P, int64_t K, int64_t c0, int rmax, bool vec,
+                             int gtid) {
+  if (vec) {
+    constexpr int CH = W / 2;
+    for (int e = gtid; e < rmax * CH; e += NTG) {
+      const int r = e / CH, cc = (e % CH) * 2;
+      if (c0 + cc < K) cp_async16(&dst[r * LD + cc], P + (int64_t)r * K + c0 + cc);
+    }
+  } else {
+    for (int e = gtid; e < rmax * W; e += NTG) {
+      const int r = e / W, cc = e % W;
+      if (c0 + cc < K) cp_async8(&dst[r * LD + cc], P + (int64_t)r * K + c0 + cc);
+    }
+  }
+  cp_async_commit();
+}
+
+// Per-row barrier of a chain CTA.  Column tiles are independent chains, so with
+// WC > 1 warp columns each column group (its WR warps) syncs on its own named
+// barrier: the groups drift apart and one group's row epilogue (stores, F-tile
+// refill, barrier) overlaps the other group's DMMAs instead of idling the pipe.
+template <int WR, int WC>
+BTD_DEVINL void group_sync(int wc) {
+  if constexpr (WC == 1) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + wc), "r"(32 * WR) : "memory");
+  }
+}
+
 template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1>
 struct ChainCfg {
   static constexpr int NW = WR * WC, NT = 32 * NW;
@@ -264,14 +287,8 @@ BTD_DEVINL void group_mma(double (&acc)[TM][TN][2], double2 (&buf)[PF][TM], cons
       b1[j] = Bs[(8 * s + 2 * t + 1) * ldb + j * 8 + g];
     }
     // all k-slot-0 products first, then k-slot-1: consecutive DMMAs are independent
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b0[j]);
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b1[j]);
+    mma_k4<TM, TN, false>(acc, a, b0);
+    mma_k4<TM, TN, true>(acc, a, b1);
   }
 }
 
@@ -383,7 +400,8 @@ __global__ void __launch_bounds__(32 * WR * WC) chain_fwd_kernel(ChainArgs a) {
     }
     // refill the slot freed by row j-1 with row j+NF-1
     if (j + NF - 1 < nint)
-      cp_tile<MP, KT, LD, NT>(Fs + ((j + NF - 1) % NF) * MP * LD, a.F + (gr + NF - 1) * rowK, K, c0, a.m, vec);
+      cp_tile_cols<Cfg::CW, LD, 32 * WR>(Fs + ((j + NF - 1) % NF) * MP * LD + cw0, a.F + (gr + NF - 1) * rowK, K,
+                                         c0 + cw0, a.m, vec, wr * 32 + lane);
     else
       cp_async_commit();
 #pragma unroll 1
@@ -401,12 +419,12 @@ __global__ void __launch_bounds__(32 * WR * WC) chain_fwd_kernel(ChainArgs a) {
           group_mma<MP, TM, TN, PF>(acc, buf, nx, Fcur + cw0, LD, grp * PF, g, t);
       }
     }
-    __syncthreads();
+    group_sync<WR, WC>(wc);
     store_smem(acc, Ys, LD, r0, cw0, g, t);
     store_tile(acc, a.X + gr * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
     zero_acc(acc);
     cp_async_wait<NF - 2>();  // row j+1's F tile has landed
-    __syncthreads();
+    group_sync<WR, WC>(wc);
   }
   cp_async_wait<0>();
   wgemm<MP, TM, TN, 2>(ser, a.Tb + (slot0 + nint - 1) * blk + r0 * MP, Ys + cw0, LD, g, t);
@@ -506,8 +524,8 @@ __global__ void __launch_bounds__(32 * WR * WC) chain_bwd_kernel(ChainArgs a) {
     if constexpr (NY > 0) {
       load_smem(acc, Ysr + (jj % NY) * MP * LD, LD, r0, cw0, g, t);
       if (jj + NY - 1 < nint)
-        cp_tile<MP, KT, LD, NT>(Ysr + ((jj + NY - 1) % NY) * MP * LD, a.X + (gr - (NY - 1)) * rowK, K, c0, a.m,
-                                vec);
+        cp_tile_cols<Cfg::CW, LD, 32 * WR>(Ysr + ((jj + NY - 1) % NY) * MP * LD + cw0, a.X + (gr - (NY - 1)) * rowK,
+                                           K, c0 + cw0, a.m, vec, wr * 32 + lane);
       else
         cp_async_commit();
     } else {
@@ -527,11 +545,11 @@ __global__ void __launch_bounds__(32 * WR * WC) chain_bwd_kernel(ChainArgs a) {
         group_mma<MP, TM, TN, PF>(acc, buf, nx, (seg == 0 ? Xq : Xn) + cw0, LD, grp * PF, g, t);
       }
     }
-    __syncthreads();
+    group_sync<WR, WC>(wc);
     store_smem(acc, Xn, LD, r0, cw0, g, t);
     store_tile(acc, a.X + gr * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
     if constexpr (NY > 1) cp_async_wait<NY - 2>();
-    __syncthreads();
+    group_sync<WR, WC>(wc);
   }
   cp_async_wait<0>();
 }
@@ -570,14 +588,8 @@ BTD_DEVINL void smem_mma(double (&acc)[TM][TN][2], const double* __restrict__ A,
       b0[j] = B[(8 * s + 2 * t) * ldb + c0 + j * 8 + g];
       b1[j] = B[(8 * s + 2 * t + 1) * ldb + c0 + j * 8 + g];
     }
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b0[j]);
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b1[j]);
+    mma_k4<TM, TN, false>(acc, a, b0);
+    mma_k4<TM, TN, true>(acc, a, b1);
   }
 }
 

@@ -25,6 +25,17 @@ BTD_DEVINL void dmma(double& c0, double& c1, double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// acc[i][j] += a[i].x (Y=0) or a[i].y (Y=1) (8x4 fragments) x b[j] (4x8): one k4 step
+// of a TM x TN warp tile, TM*TN independent DMMAs back to back.  (mma.m16n8k4.f64
+// is no wider on sm_100a: ptxas lowers it to two DMMA.8x8x4, checked in the SASS.)
+template <int TM, int TN, bool Y>
+BTD_DEVINL void mma_k4(double (&acc)[TM][TN][2], const double2 (&a)[TM], const double (&b)[TN]) {
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], Y ? a[i].y : a[i].x, b[j]);
+}
+
 BTD_DEVINL unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }

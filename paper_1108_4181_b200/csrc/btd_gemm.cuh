@@ -178,14 +178,8 @@ __global__ void __launch_bounds__(32 * WGM * WGN) gemm_pipe_kernel(GemmDesc d) {
             b0[j] = Bs[(8 * s + 2 * t) * LDB + wn * C_::WTN + j * 8 + g];
             b1[j] = Bs[(8 * s + 2 * t + 1) * LDB + wn * C_::WTN + j * 8 + g];
           }
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b0[j]);
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b1[j]);
+          mma_k4<TM, TN, false>(acc, a, b0);
+          mma_k4<TM, TN, true>(acc, a, b1);
         }
       }
       cp_async_wait<0>();
@@ -328,14 +322,8 @@ __global__ void __launch_bounds__(32 * (WGM * WGN + 1), 1) gemm_ws_kernel(GemmDe
             b0[j] = Bs[(8 * s + 2 * t) * LDB + wn * C_::WTN + j * 8 + g];
             b1[j] = Bs[(8 * s + 2 * t + 1) * LDB + wn * C_::WTN + j * 8 + g];
           }
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b0[j]);
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b1[j]);
+          mma_k4<TM, TN, false>(acc, a, b0);
+          mma_k4<TM, TN, true>(acc, a, b1);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[sl]);
@@ -501,14 +489,8 @@ __global__ void __launch_bounds__(32 * (WGM * WGN + 1), 1)
             b0[j] = Bb[k_0 * 16 + ((ch ^ (k_0 & 7)) << 1) + e];
             b1[j] = Bb[(k_0 + 1) * 16 + ((ch ^ ((k_0 + 1) & 7)) << 1) + e];
           }
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b0[j]);
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b1[j]);
+          mma_k4<TM, TN, false>(acc, a, b0);
+          mma_k4<TM, TN, true>(acc, a, b1);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[sl]);

@@ -63,14 +63,8 @@ BTD_DEVINL void gmem_mma(double (&acc)[TM][TN][2], const double* __restrict__ A,
       b0[j] = c < K ? __ldcg(B + (int64_t)(8 * s + 2 * t) * ldb + j * 8 + g) : 0.0;
       b1[j] = c < K ? __ldcg(B + (int64_t)(8 * s + 2 * t + 1) * ldb + j * 8 + g) : 0.0;
     }
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b0[j]);
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b1[j]);
+    mma_k4<TM, TN, false>(acc, a, b0);
+    mma_k4<TM, TN, true>(acc, a, b1);
   }
 }
 
@@ -97,14 +91,8 @@ struct BlkFrag {
   BTD_DEVINL void mma(double (&acc)[TM][TN][2]) const {
 #pragma unroll
     for (int s = 0; s < MP / 8; ++s) {
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[s][i].x, b0[s][j]);
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[s][i].y, b1[s][j]);
+    mma_k4<TM, TN, false>(acc, a[s], b0[s]);
+    mma_k4<TM, TN, true>(acc, a[s], b1[s]);
     }
   }
 };
