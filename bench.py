@@ -316,6 +316,11 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one GPU per rank (LOCAL_RANK); BTD_DIST_BACKEND=gloo (host collectives) lets the
+    # multi-rank flow run with several ranks on one device for functional checks --
+    # no kernel waits on another rank, the exchanges go through the host
+    backend = os.environ.get("BTD_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     sharded = world > 1 or args.sharded
@@ -324,7 +329,8 @@ def run_b200(args):
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        dist.init_process_group(backend, rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local) if backend == "nccl" else None)
     from paper_1108_4181_b200 import _native, configs, plan_build_arrays
     from paper_1108_4181_b200.distributed import ShardedPlan
 
@@ -405,8 +411,9 @@ def run_b200(args):
     ph = [buf[i] / max(1, nsv.value) for i in range(4)]
 
     res = None
-    if not args.no_check and not sharded:
-        res = residual_check(torch, name, X, F, configs)
+    if not args.no_check:
+        res = (residual_check_sharded(torch, dist, name, X, F, configs, row_lo, row_hi) if sharded
+               else residual_check(torch, name, X, F, configs))
 
     # e2e through the host-memory API: pinned host F -> device -> solve -> host X
     e2e = None
@@ -526,6 +533,35 @@ def residual_check(torch, name, X, F, configs):
     del diag, lower, upper, y
     torch.cuda.empty_cache()
     return r
+
+
+def residual_check_sharded(torch, dist, name, X, F, configs, lo, hi):
+    """Sharded form of residual_check: each rank's rows [lo, hi) with the neighbour
+    ranks' boundary rows of X exchanged (one all-gather of first/last rows); the
+    max over ranks of max|P X - F| over the max over ranks of max|F|."""
+    diag, lower, upper, _ = configs.generate(name, device="cuda", k=0)
+    n = diag.shape[0]
+    world, rank = dist.get_world_size(), dist.get_rank()
+    edge = torch.stack([X[0], X[-1]]).contiguous()
+    edges = torch.empty((2 * world,) + tuple(X.shape[1:]), dtype=X.dtype, device=X.device)
+    dist.all_gather_into_tensor(edges, edge)
+    edges = edges.view((world, 2) + tuple(X.shape[1:]))
+    y = torch.bmm(diag[lo:hi], X)
+    if lo >= 1:  # row i reads -lower[i-1] x_{i-1}
+        xm = torch.cat([edges[rank - 1, 1:2], X[:-1]])
+        y -= torch.bmm(lower[lo - 1:hi - 1], xm)
+    elif hi - lo > 1:
+        y[1:] -= torch.bmm(lower[0:hi - 1], X[:-1])
+    if hi <= n - 1:  # row i reads -upper[i] x_{i+1}
+        xp = torch.cat([X[1:], edges[rank + 1, 0:1]])
+        y -= torch.bmm(upper[lo:hi], xp)
+    elif hi - lo > 1:
+        y[:-1] -= torch.bmm(upper[lo:hi - 1], X[1:])
+    t = torch.tensor([(y - F).abs().max().item(), F.abs().max().item()], dtype=torch.float64, device=X.device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    del diag, lower, upper, y
+    torch.cuda.empty_cache()
+    return float(t[0] / t[1])
 
 
 def run_dd(args):
