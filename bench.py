@@ -81,6 +81,26 @@ CPU_SAMPLE = {
 }
 
 
+_OUT = None
+
+
+def emit(line):
+    """The one JSON result line, on the process's original stdout."""
+    print(json.dumps(line), file=_OUT or sys.stdout, flush=True)
+
+
+def _stdout_to_stderr():
+    """Native libraries (NCCL's version banner, CUDA) may print to fd 1; keep stdout
+    for the JSON line alone by pointing fd 1 at stderr and emitting through a dup."""
+    global _OUT
+    try:
+        sys.stdout.flush()
+        _OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+    except OSError:
+        _OUT = None
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -304,7 +324,7 @@ def run_reference(args):
         "cpu_baseline": {"value": value, "unit": "RHS/s", "cores": cs.cores, "kind": "port", "sample": cs.sample},
         "e2e": {"value": value, "unit": "RHS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # --------------------------------------------------------------------------- GPU arm
@@ -428,9 +448,7 @@ def run_b200(args):
                     _native.check(st)
         else:
             def solve_host():
-                F.copy_(Fh, non_blocking=True)
-                Xh.copy_(plan.solve(F, out=X), non_blocking=True)
-                torch.cuda.current_stream().synchronize()
+                plan.solve_host(Fh, Xh)
         solve_host()
         torch.cuda.synchronize()
         if dist:
@@ -508,7 +526,7 @@ def run_b200(args):
         "clocks": clocks,
         "gpu_launches": launches,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     if dist:
         dist.destroy_process_group()
 
@@ -607,7 +625,7 @@ def run_dd(args):
                                "frac": flops / (fp64 * 1e12) * 1e3 / ms, "fp64_tflops_peak": fp64},
             "plan_build_s": build_s, "grid_rel_residual": res, "clocks": clk.summary(),
             "gpu_launches": _native.launch_count() - lc0}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main():
@@ -624,6 +642,7 @@ def main():
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use the row-sharded NCCL path even on one GPU")
     args = ap.parse_args()
+    _stdout_to_stderr()
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "c3dd":

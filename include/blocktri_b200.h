@@ -172,6 +172,14 @@ int btd_shard_solve_c(btd_plan* plan, const double* partial_all, const double* f
 int btd_plan_set_profiling(btd_plan* plan, int enable);
 int btd_plan_phase_times(btd_plan* plan, double* ms_out, int64_t* nsolves, int reset);
 
+/* Column-chunk copy between an (rows, K) host array and a dense (rows, kc)
+ * device chunk, stream-ordered (cudaMemcpy2DAsync; the per-rank host pipeline
+ * of the sharded solve, ShardedPlan.solve_host).  to_device = 1: host columns
+ * [c0, c0+kc) -> device; 0: device -> host columns.  Host memory should be
+ * pinned to overlap with compute. */
+int btd_copy_columns(double* host, int64_t rows, int64_t K, int64_t c0, int64_t kc, double* dev, int to_device,
+                     void* stream);
+
 /* Kernel launches issued by this library since load (the bench's
  * gpu_launches evidence) and the last error text. */
 int64_t btd_launch_count(void);

@@ -50,6 +50,7 @@ EXPORTS = (
     "btd_shard_solve_c",
     "btd_plan_set_profiling",
     "btd_plan_phase_times",
+    "btd_copy_columns",
     "btd_launch_count",
     "btd_last_error",
     "btd_version",
@@ -123,6 +124,8 @@ def load():
     lib.btd_plan_set_profiling.restype = i32
     lib.btd_plan_phase_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64), i32]
     lib.btd_plan_phase_times.restype = i32
+    lib.btd_copy_columns.argtypes = [dp, i64, i64, i64, i64, dp, i32, vp]
+    lib.btd_copy_columns.restype = i32
     lib.btd_launch_count.argtypes = []
     lib.btd_launch_count.restype = i64
     lib.btd_last_error.argtypes = []

@@ -1827,6 +1827,23 @@ int btd_band_from_probes(const double* y, int64_t n, int64_t d, int64_t ldy, dou
   }
   return BTD_OK;
 }
+int btd_copy_columns(double* host, int64_t rows, int64_t K, int64_t c0, int64_t kc, double* dev, int to_device,
+                     void* stream) {
+  if (!host || !dev || rows < 0 || kc < 1 || c0 < 0 || c0 + kc > K) {
+    g_err = "btd_copy_columns: bad arguments";
+    return BTD_ERR_INVALID_ARG;
+  }
+  if (rows == 0) return BTD_OK;
+  const size_t w = (size_t)kc * sizeof(double), hp = (size_t)K * sizeof(double);
+  const cudaError_t e =
+      to_device ? cudaMemcpy2DAsync(dev, w, host + c0, hp, w, (size_t)rows, cudaMemcpyHostToDevice, (cudaStream_t)stream)
+                : cudaMemcpy2DAsync(host + c0, hp, dev, w, w, (size_t)rows, cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    g_err = std::string("btd_copy_columns: ") + cudaGetErrorString(e);
+    return BTD_ERR_CUDA;
+  }
+  return BTD_OK;
+}
 int64_t btd_launch_count(void) { return g_launches.load(); }
 const char* btd_last_error(void) { return g_err.c_str(); }
 

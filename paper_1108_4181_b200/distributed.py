@@ -121,6 +121,12 @@ class NativeBackend:
             _native.check(self.lib.btd_shard_solve_c(h, self._p(partial_all), self._p(f_local), self._p(x_local), k,
                                                      self._stream()))
 
+    def copy_columns(self, host, c0, kc, dev, to_device, stream):
+        """host (rows, m, K) pinned CPU tensor columns [c0, c0+kc) <-> dense device chunk."""
+        rows = int(host.shape[0]) * int(host.shape[1])
+        _native.check(self.lib.btd_copy_columns(self._p(host), rows, int(host.shape[2]), c0, kc, self._p(dev),
+                                                1 if to_device else 0, ctypes.c_void_p(stream.cuda_stream)))
+
     def destroy(self, h):
         self.lib.btd_plan_destroy(h)
 
@@ -234,6 +240,46 @@ class ShardedPlan:
             self._gather(part_all, part[:npart], "partial", trace, npart * 8, cap)
         self.be.solve_c(self.h, part_all, f_local, x_local, k)
         return x_local
+
+    def solve_host(self, f_host, x_host, chunks=4):
+        """Host-buffer solve of this shard (the reference's numpy-in / numpy-out
+        contract, per rank): K columns in ``chunks`` column chunks through an
+        H2D stream -> the solve (current stream, with its two all-gathers) -> a
+        D2H stream, so chunk c+1's copy-in and chunk c-1's copy-out overlap chunk
+        c's solve (the sharded counterpart of ``btd_plan_solve_host``).  f_host /
+        x_host: pinned CPU tensors (row_hi - row_lo, m, K); returns x_host."""
+        torch = self.be.torch
+        rows, m, k = (int(v) for v in f_host.shape)
+        nch = max(1, min(int(chunks), k))
+        while k % nch or ((k // nch) % 2 and nch > 1):
+            nch -= 1
+        kc = k // nch
+        dev = torch.device("cuda", torch.cuda.current_device())
+        comp = torch.cuda.current_stream()
+        if not hasattr(self, "_hstreams"):
+            self._hstreams = (torch.cuda.Stream(), torch.cuda.Stream())
+        s_in, s_out = self._hstreams
+        nbuf = min(nch, 3)
+        bufs = [torch.empty((rows, m, kc), dtype=torch.float64, device=dev) for _ in range(nbuf)]
+        ev_in = [torch.cuda.Event() for _ in range(nch)]
+        ev_sol = [torch.cuda.Event() for _ in range(nch)]
+        ev_out = [torch.cuda.Event() for _ in range(nch)]
+        s_in.wait_stream(comp)
+        for c in range(nch):
+            b = bufs[c % nbuf]
+            if c >= nbuf:
+                s_in.wait_event(ev_out[c - nbuf])  # buffer free again
+            self.be.copy_columns(f_host, c * kc, kc, b, True, s_in)
+            ev_in[c].record(s_in)
+            comp.wait_event(ev_in[c])
+            self.solve(b, out=b)
+            ev_sol[c].record(comp)
+            s_out.wait_event(ev_sol[c])
+            self.be.copy_columns(x_host, c * kc, kc, b, False, s_out)
+            ev_out[c].record(s_out)
+        comp.wait_stream(s_out)
+        s_out.synchronize()
+        return x_host
 
     def collectives_per_solve(self, k=1):
         """1 (carry) or 2 (carry + crossing-node partial sums) all-gathers per solve."""

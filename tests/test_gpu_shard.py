@@ -134,6 +134,13 @@ def test_sharded_plan_over_nccl_world1():
         x = plan.solve(torch.from_numpy(f).cuda(), trace=tr).cpu().numpy()
         assert tr.stages == 0 and len(tr.timings) == plan.collectives_per_solve(16)  # NCCL timed by events
         assert all(ms >= 0 for _label, ms in tr.timings)
+        # pipelined host-buffer solve (column chunks through H2D / solve / D2H streams)
+        fh = torch.from_numpy(f).pin_memory()
+        for chunks in (1, 4, 8):
+            xh = torch.zeros_like(fh).pin_memory()
+            plan.solve_host(fh, xh, chunks=chunks)
+            # columns are independent; only the tree's split-K segmentation may depend on the width
+            assert O.max_rel_err(xh.numpy(), x) <= 1e-12
         plan.close()
     finally:
         dist.destroy_process_group()
