@@ -58,15 +58,30 @@ BENCH_CFG = {
     # Helmholtz DD; P = 9 ranges of 7 interface rows on one GPU (288 GEMM tiles fill the
     # 296 CTA slots), P = 8 (a multiple of 2/4/8) when sharded
     "c3": dict(subdomains_per_gpu=lambda w: 9 if w == 1 else 8 // w, ranges_per_gpu=1),
-    "c4": dict(subdomains_per_gpu=lambda w: 8 * w, ranges_per_gpu=592),
+    # c4: 592 = 4 x 148 device ranges per GPU (one wave of the 4-CTA/SM streamed sweeps);
+    # split = floor(592 / subdomains per GPU): 74 / 37 / 18 / 9 on 1 / 2 / 4 / 8 GPUs (one
+    # wave, shallow sharded trees; tools/shard_projection.py, profiles/r01_shard_projection.txt)
+    "c4": dict(subdomains_per_gpu=lambda w: 8 * w, ranges_per_gpu=592, one_wave=True),
 }
 
 
 def plan_params(name, world, ranks=0, split=0):
+    """(ranks, split): split = the smallest second-level factor with at least
+    ranges_per_gpu device ranges per GPU that are a whole multiple of it (the
+    sweep grids are whole waves: c4 at 32 subdomains/GPU -> split 37, 1184
+    ranges, not split 19 -> 608 ranges = 4.1 waves; profiles/r01_ab_bwd.txt)."""
     bc = BENCH_CFG[name]
     spg = bc["subdomains_per_gpu"](world)
     r = ranks or spg * world
-    sp = split or max(1, -(-bc["ranges_per_gpu"] // spg))
+    if split:
+        return r, split
+    rpg = bc["ranges_per_gpu"]
+    if bc.get("one_wave"):
+        return r, max(1, rpg // spg)
+    sp = max(1, -(-rpg // spg))
+    if rpg > 1:
+        while (spg * sp) % rpg:
+            sp += 1
     return r, sp
 
 

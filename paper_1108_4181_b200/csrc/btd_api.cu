@@ -437,6 +437,10 @@ struct btd_plan {
   };
   int64_t partial_elems_per_k = 0;  // split-K scratch: doubles per unit K
   DevBuf partial;
+  // fused cooperative tree for a row-sharded plan (M <= 32, world > 1): phases B and C
+  bool fused_shard = false;
+  ShardTreeArgs sargs{};
+  int shard_chunks = 0, shard_work_b = 0, shard_work_c = 0;
   // fused cooperative tree (M <= 32, single rank)
   bool fused_tree = false;
   TreeArgs targs{};
@@ -745,8 +749,10 @@ void launch_chain(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
       else if (variant == 16) launch_chain_t<64, 128, 8, 4, 2, 0>(a, fwd, st);
       else if (variant == 17) launch_chain_t<64, 64, 8, 2, 2, 0>(a, fwd, st);
       else if (variant == 18) launch_chain_t<64, 64, 4, 2, 2, 0>(a, fwd, st);
-      else if (fwd) launch_chain_t<64, 128, 8, 2, 2, 0>(a, fwd, st);  // measured best (c2): wide tiles forward,
-      else launch_chain_t<64, 32, 8, 1, 3, 0>(a, fwd, st);             // narrow register-prefetch tiles backward
+      else if (variant == 19) launch_chain_t<64, 64, 8, 1, 2, 0>(a, fwd, st);
+      // measured best (c2, profiles/r01_ab_bwd.txt): 128-column tiles of 2 x 8 warps with
+      // per-column-group barriers in both directions (bwd 9.96 -> 9.54 ms vs 32-column tiles)
+      else launch_chain_t<64, 128, 8, 2, 2, 0>(a, fwd, st);
       break;
     case 128:
       if (variant == 1) launch_chain_t<128, 64, 16, 2>(a, fwd, st);
@@ -1392,6 +1398,63 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
       pl.tree_chunks = ta.nchunks;
       pl.fused_tree = true;
     }
+    if (pl.mode == 0 && mp <= 32 && (!ft_env || atoi(ft_env))) {  // (a world-1 shard plan uses it too)
+      constexpr int CH = 16;
+      std::vector<int64_t> cro_, crld_, cflo_, odst, klist(nn), xlv(nn), xhv(nn);
+      std::vector<int32_t> cnb_, ooff, ocnt, he(nn, 0), hh(nn, 0), lvo, lvn;
+      auto add_out = [&](int64_t dst, int64_t r0, int64_t ld, int64_t f0, int64_t nblk) {
+        ooff.push_back((int32_t)cro_.size());
+        for (int64_t b0 = 0; b0 < nblk; b0 += CH) {
+          cro_.push_back(r0 + b0 * mp); crld_.push_back(ld); cflo_.push_back(f0 + b0);
+          cnb_.push_back((int32_t)std::min<int64_t>(CH, nblk - b0));
+        }
+        ocnt.push_back((int32_t)cro_.size() - ooff.back());
+        odst.push_back(dst);
+      };
+      for (int b = 0; b < nn; ++b)  // nodes inside this rank: full series sums
+        if (need_k[pl.nodes[b].k] && !crossing[b]) add_out(b, roff[b], rld[b], pl.nodes[b].lo, sz[b]);
+      int64_t ci = 0;
+      for (int b = 0; b < nn; ++b) {  // crossing nodes: this rank's share (same order as cross_node)
+        if (!crossing[b]) continue;
+        const Node& nd = pl.nodes[b];
+        const int64_t a = std::max(nd.lo, pl.q0), e = std::min(nd.hi, pl.q1 - 1);
+        add_out(-1 - ci, roff[b] + std::max<int64_t>(0, a - nd.lo) * mp, rld[b], a, a <= e ? e - a + 1 : 0);
+        ++ci;
+      }
+      for (int b = 0; b < nn; ++b) {
+        const Node& nd = pl.nodes[b];
+        klist[b] = nd.k;
+        xlv[b] = nd.lo >= 1 ? nd.lo - 1 : nr;
+        xhv[b] = nd.hi + 1 <= nr - 1 ? nd.hi + 1 : nr;
+        he[b] = nd.lo >= 1;
+        hh[b] = nd.hi + 1 <= nr - 1;
+      }
+      for (int64_t lev = 0; lev <= maxlevel; ++lev) {
+        lvo.push_back((int32_t)lvn.size());
+        for (int b = 0; b < nn; ++b)
+          if (pl.nodes[b].level == lev && need_k[pl.nodes[b].k]) lvn.push_back(b);
+      }
+      lvo.push_back((int32_t)lvn.size());
+      ShardTreeArgs& sa = pl.sargs;
+      sa.nchunks = (int)cro_.size();
+      sa.nout = (int)odst.size();
+      sa.ncross = pl.ncross;
+      sa.nlev = (int)maxlevel + 1;
+      sa.world = pl.world;
+      sa.ch_roff = pl.upload(cro_); sa.ch_rld = pl.upload(crld_); sa.ch_flo = pl.upload(cflo_);
+      sa.ch_nblk = pl.upload(cnb_);
+      sa.out_off = pl.upload(ooff); sa.out_cnt = pl.upload(ocnt); sa.out_dst = pl.upload(odst);
+      sa.cross_node = pl.cross_node;
+      sa.lv_off = pl.upload(lvo); sa.lv_nodes = pl.upload(lvn);
+      sa.k = pl.upload(klist); sa.xl = pl.upload(xlv); sa.xh = pl.upload(xhv);
+      sa.has_e = pl.upload(he); sa.has_h = pl.upload(hh);
+      int maxlev = 0;
+      for (size_t l = 0; l + 1 < lvo.size(); ++l) maxlev = std::max(maxlev, lvo[l + 1] - lvo[l]);
+      pl.shard_chunks = std::max(sa.nchunks, 1);
+      pl.shard_work_b = std::max(sa.nchunks, sa.nout);
+      pl.shard_work_c = std::max(pl.ncross, maxlev);
+      pl.fused_shard = true;
+    }
   }
   CK(cudaStreamSynchronize(st));
   pl.factor_bytes += (int64_t)(rtot + 2 * nn * blk) * sizeof(double);
@@ -1412,7 +1475,8 @@ void ensure_scratch(btd_plan& pl, int64_t K) {
   S.xt.alloc((size_t)(pl.nr + 1) * mpK * sizeof(double));
   CK(cudaMemset(S.xt.p, 0, (size_t)(pl.nr + 1) * mpK * sizeof(double)));
   CK(cudaMemset(S.ft.p, 0, (size_t)pl.nr * mpK * sizeof(double)));
-  if (pl.fused_tree) S.tpartial.alloc((size_t)std::max(pl.tree_chunks, 1) * pl.mp * K * sizeof(double));
+  if (pl.fused_tree || pl.fused_shard)
+    S.tpartial.alloc((size_t)std::max({pl.tree_chunks, pl.shard_chunks, 1}) * pl.mp * K * sizeof(double));
   if (pl.partial_elems_per_k) S.partial.alloc((size_t)pl.partial_elems_per_k * K * sizeof(double));
   S.k = K;
 }
@@ -1516,6 +1580,43 @@ void launch_tree_small(btd_plan& pl, int64_t K, cudaStream_t st) {
   void* args[] = {&ta};
   CK(cudaLaunchCooperativeKernel((const void*)tree_small_kernel<MP>, dim3(grid), dim3(256), args, 0, st));
   CK_LAUNCH();
+}
+
+// Sharded fused tree: phase B (series sums + crossing partials) or C (crossing sums + levels).
+template <int MP>
+void launch_tree_shard(btd_plan& pl, int64_t K, bool phase_b, double* part_out, const double* part_all,
+                       cudaStream_t st) {
+  const void* fn = phase_b ? (const void*)tree_shard_b_kernel<MP> : (const void*)tree_shard_c_kernel<MP>;
+  int max_blocks = 0, nsm = 0, dev = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks, fn, 256, 0));
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  ShardTreeArgs sa = pl.sargs;
+  sa.K = K;
+  sa.R = pl.Rrows.d();
+  sa.EH = pl.EH.d();
+  sa.ft = pl.S().ft.d();
+  sa.partial = pl.S().tpartial.d();
+  sa.z = pl.S().zbuf.d();
+  sa.xt = pl.S().xt.d();
+  sa.part_out = part_out;
+  sa.part_all = part_all;
+  const int ntile = (int)((K + 15) / 16);
+  const int64_t work = (int64_t)std::max(phase_b ? pl.shard_work_b : pl.shard_work_c, 1) * ntile;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)max_blocks * nsm, (work + 7) / 8));
+  void* args[] = {&sa};
+  CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, 0, st));
+  CK_LAUNCH();
+}
+
+void tree_shard(btd_plan& pl, int64_t K, bool phase_b, double* part_out, const double* part_all,
+                cudaStream_t st) {
+  switch (pl.mp) {
+    case 8: launch_tree_shard<8>(pl, K, phase_b, part_out, part_all, st); break;
+    case 16: launch_tree_shard<16>(pl, K, phase_b, part_out, part_all, st); break;
+    case 32: launch_tree_shard<32>(pl, K, phase_b, part_out, part_all, st); break;
+    default: fail(BTD_ERR_UNSUPPORTED, "fused shard tree: block order > 32");
+  }
 }
 
 // Algorithm 1 on the interface system: z = R f~ (all needed nodes), then the levels.
@@ -1675,6 +1776,10 @@ void solve_shard_b(btd_plan& pl, const double* carry_all, double* partial_out, i
     add_block_kernel<<<64, 256, 0, st>>>(ft + pl.q0 * mpK, carry_all + (int64_t)(pl.rank - 1) * mpK, mpK);
     CK_LAUNCH();
   }
+  if (pl.fused_shard) {
+    tree_shard(pl, K, true, partial_out, nullptr, st);
+    return;
+  }
   launch_gemm(mp, K, pl.nz, mk(pl.S().zbuf.d(), pl.z_id, 0, mpK, K), none(), 0.0,
               {z_term(pl, ft, K)}, st,
               split_with(pl.z_split, pl));
@@ -1687,6 +1792,13 @@ void solve_shard_b(btd_plan& pl, const double* carry_all, double* partial_out, i
 // Sharded phase C: crossing-node sums, tree levels, local recovery.
 void solve_shard_c(btd_plan& pl, const double* partial_all, const double* F, double* X, int64_t K, cudaStream_t st) {
   const int64_t mp = pl.mp, mpK = mp * K;
+  if (pl.fused_shard) {
+    tree_shard(pl, K, false, nullptr, partial_all, st);
+    pl.ev_mark(st);
+    solve_backward(pl, F, X, K, st);
+    pl.ev_mark(st);
+    return;
+  }
   if (pl.ncross) {
     dim3 grid((unsigned)std::min<int64_t>((mpK + 255) / 256, 64), (unsigned)std::min(pl.ncross, 65535));
     sum_ranks_kernel<<<grid, 256, 0, st>>>(partial_all, pl.world, pl.ncross, mpK, pl.cross_node, pl.S().zbuf.d());

@@ -97,6 +97,34 @@ struct BlkFrag {
   }
 };
 
+// acc = sum over nblk consecutive blocks e of R[:, e] (MP x MP at column e*MP of a
+// row-major MP x ld array) times f~ block e (MP x 16 columns from col0; blocks
+// MP*K apart) -- one chunk of a series sum, blocks added in order.
+template <int MP, int TM, int TN>
+BTD_DEVINL void chunk_series_sum(double (&acc)[TM][TN][2], const double* __restrict__ Rb, int64_t ld,
+                                 const double* __restrict__ Fb, int nblk, int64_t K, int64_t col0, int g, int t) {
+  const int64_t mpK = (int64_t)MP * K;
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if constexpr (MP >= 32) {  // two fragment sets would not fit the register budget
+    for (int e = 0; e < nblk; ++e) gmem_mma<MP, TM, TN>(acc, Rb + e * MP, ld, Fb + e * mpK, K, col0, K, g, t);
+  } else {
+    // block e+1's fragments are in flight while block e's products run (same order of sums)
+    BlkFrag<MP, TM, TN> fa, fb;
+    fa.load(Rb, ld, Fb, K, col0, K, g, t);
+    int e = 0;
+    for (; e + 1 < nblk; e += 2) {
+      fb.load(Rb + (e + 1) * MP, ld, Fb + (e + 1) * mpK, K, col0, K, g, t);
+      fa.mma(acc);
+      if (e + 2 < nblk) fa.load(Rb + (e + 2) * MP, ld, Fb + (e + 2) * mpK, K, col0, K, g, t);
+      fb.mma(acc);
+    }
+    if (e < nblk) fa.mma(acc);
+  }
+}
+
 template <int TM, int TN>
 BTD_DEVINL void acc_add_tile(double (&acc)[TM][TN][2], const double* __restrict__ P, int64_t K, int64_t col0, int g,
                              int t) {
@@ -158,32 +186,8 @@ __global__ void __launch_bounds__(256) tree_small_kernel(TreeArgs a) {
     const int64_t col0 = (int64_t)(item % ntile) * 16;
     const int b = a.ch_node[c];
     double acc[TM][TN][2];
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    const int64_t ld = a.rld[b];
-    const int nblk = a.ch_nblk[c];
-    const int64_t bk0 = a.ch_blk0[c];
-    const double* Rb = a.R + a.roff[b];
-    const double* Fb = a.ft + a.lo[b] * mpK + col0;
-    if constexpr (MP >= 32) {  // two fragment sets would not fit the register budget
-      for (int e = 0; e < nblk; ++e)
-        gmem_mma<MP, TM, TN>(acc, Rb + (bk0 + e) * MP, ld, Fb + (bk0 + e) * mpK, K, col0, K, g, t);
-      acc_store_tile(acc, a.partial + (int64_t)c * mpK, K, col0, g, t);
-      continue;
-    }
-    // block e+1's fragments are in flight while block e's products run (same order of sums)
-    BlkFrag<MP, TM, TN> fa, fb;
-    fa.load(Rb + bk0 * MP, ld, Fb + bk0 * mpK, K, col0, K, g, t);
-    int e = 0;
-    for (; e + 1 < nblk; e += 2) {
-      fb.load(Rb + (bk0 + e + 1) * MP, ld, Fb + (bk0 + e + 1) * mpK, K, col0, K, g, t);
-      fa.mma(acc);
-      if (e + 2 < nblk) fa.load(Rb + (bk0 + e + 2) * MP, ld, Fb + (bk0 + e + 2) * mpK, K, col0, K, g, t);
-      fb.mma(acc);
-    }
-    if (e < nblk) fa.mma(acc);
+    chunk_series_sum<MP, TM, TN>(acc, a.R + a.roff[b] + (int64_t)a.ch_blk0[c] * MP, a.rld[b],
+                                 a.ft + (a.lo[b] + a.ch_blk0[c]) * mpK + col0, a.ch_nblk[c], K, col0, g, t);
     acc_store_tile(acc, a.partial + (int64_t)c * mpK, K, col0, g, t);
   }
   grid.sync();
@@ -219,6 +223,127 @@ __global__ void __launch_bounds__(256) tree_small_kernel(TreeArgs a) {
         }
         for (; c < ncnt; ++c) acc_add_tile(acc, P0 + (int64_t)c * mpK, K, col0, g, t);
       }
+      if (a.has_e[b])
+        gmem_mma<MP, TM, TN>(acc, a.EH + (2 * (int64_t)b) * blk, MP, a.xt + a.xl[b] * mpK + col0, K, col0, K, g, t);
+      if (a.has_h[b])
+        gmem_mma<MP, TM, TN>(acc, a.EH + (2 * (int64_t)b + 1) * blk, MP, a.xt + a.xh[b] * mpK + col0, K, col0, K, g,
+                             t);
+      acc_store_tile(acc, a.xt + a.k[b] * mpK, K, col0, g, t);
+    }
+    grid.sync();
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Fused Algorithm 1 for a row-sharded plan (M <= 32, one rank of `world`).
+// The rank's needed tree nodes split into nodes inside its own ranges (series
+// sums computed here) and crossing nodes (each rank contributes the partial sum
+// over its own ranges; the partials are all-gathered and added in rank order).
+//   phase B (one cooperative launch, before the partials all-gather):
+//     chunk partials of every inside node and of this rank's share of every
+//     crossing node; grid sync; outputs: z_b (inside nodes) and part_out[c]
+//     (crossing index c, zero when the rank owns none of its segment).
+//   phase C (one cooperative launch, after it):
+//     z_node(c) = sum_r part_all[r][c] (fixed rank order); grid sync; the levels
+//     x~_k = z + E x~ + H x~ over this rank's needed nodes, one grid sync each.
+// Same per-node arithmetic as the per-level GEMM path (ref dichotomy.py:279-295).
+struct ShardTreeArgs {
+  int nchunks, nout, ncross, nlev, world;
+  int64_t K;
+  const int64_t* ch_roff;  // chunk: first R element, R row stride, first f~ range, blocks
+  const int64_t* ch_rld;
+  const int64_t* ch_flo;
+  const int32_t* ch_nblk;
+  const int32_t* out_off;  // output o sums chunks [out_off, out_off + out_cnt)
+  const int32_t* out_cnt;
+  const int64_t* out_dst;  // >= 0: node index into z; < 0: -(1 + crossing index) into part_out
+  const int64_t* cross_node;
+  const int32_t* lv_off;
+  const int32_t* lv_nodes;
+  const int64_t* k;
+  const int64_t* xl;
+  const int64_t* xh;
+  const int32_t* has_e;
+  const int32_t* has_h;
+  const double* R;
+  const double* EH;
+  const double* ft;
+  double* partial;  // [nchunks][MP][K]
+  double* z;        // [nodes][MP][K]
+  double* xt;       // [nr+1][MP][K]
+  double* part_out;        // [ncross][MP][K]
+  const double* part_all;  // [world][ncross][MP][K]
+};
+
+template <int MP>
+__global__ void __launch_bounds__(256) tree_shard_b_kernel(ShardTreeArgs a) {
+  namespace cg = cooperative_groups;
+  constexpr int TM = MP / 8, TN = 2;
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  const int64_t K = a.K, mpK = (int64_t)MP * K;
+  const int ntile = (int)((K + 15) / 16);
+  for (int item = gw; item < a.nchunks * ntile; item += nw) {
+    const int c = item / ntile;
+    const int64_t col0 = (int64_t)(item % ntile) * 16;
+    double acc[TM][TN][2];
+    chunk_series_sum<MP, TM, TN>(acc, a.R + a.ch_roff[c], a.ch_rld[c], a.ft + a.ch_flo[c] * mpK + col0,
+                                 a.ch_nblk[c], K, col0, g, t);
+    acc_store_tile(acc, a.partial + (int64_t)c * mpK, K, col0, g, t);
+  }
+  grid.sync();
+  for (int item = gw; item < a.nout * ntile; item += nw) {
+    const int o = item / ntile;
+    const int64_t col0 = (int64_t)(item % ntile) * 16;
+    double acc[TM][TN][2];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const double* P0 = a.partial + (int64_t)a.out_off[o] * mpK;
+    for (int c = 0; c < a.out_cnt[o]; ++c) acc_add_tile(acc, P0 + (int64_t)c * mpK, K, col0, g, t);
+    const int64_t d = a.out_dst[o];
+    double* dst = d >= 0 ? a.z + d * mpK : a.part_out + (-1 - d) * mpK;
+    acc_store_tile(acc, dst, K, col0, g, t);
+  }
+}
+
+template <int MP>
+__global__ void __launch_bounds__(256) tree_shard_c_kernel(ShardTreeArgs a) {
+  namespace cg = cooperative_groups;
+  constexpr int TM = MP / 8, TN = 2;
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  const int64_t K = a.K, mpK = (int64_t)MP * K;
+  const int ntile = (int)((K + 15) / 16);
+  constexpr int64_t blk = (int64_t)MP * MP;
+  if (a.ncross) {
+    for (int item = gw; item < a.ncross * ntile; item += nw) {
+      const int c = item / ntile;
+      const int64_t col0 = (int64_t)(item % ntile) * 16;
+      double acc[TM][TN][2];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int r = 0; r < a.world; ++r)
+        acc_add_tile(acc, a.part_all + ((int64_t)r * a.ncross + c) * mpK, K, col0, g, t);
+      acc_store_tile(acc, a.z + a.cross_node[c] * mpK, K, col0, g, t);
+    }
+    grid.sync();
+  }
+  for (int l = 0; l < a.nlev; ++l) {
+    const int n0 = a.lv_off[l], n1 = a.lv_off[l + 1];
+    for (int item = gw; item < (n1 - n0) * ntile; item += nw) {
+      const int b = a.lv_nodes[n0 + item / ntile];
+      const int64_t col0 = (int64_t)(item % ntile) * 16;
+      double acc[TM][TN][2];
+      acc_load_tile(acc, a.z + (int64_t)b * mpK, K, col0, g, t);
       if (a.has_e[b])
         gmem_mma<MP, TM, TN>(acc, a.EH + (2 * (int64_t)b) * blk, MP, a.xt + a.xl[b] * mpK + col0, K, col0, K, g, t);
       if (a.has_h[b])

@@ -81,12 +81,19 @@ def _emulate(d, lo, up, f, ranks, split, world, reimport=False):
     return ("ok", x)
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("n,m,k,ranks,split", [(256, 16, 8, 8, 1), (203, 8, 5, 4, 3), (96, 64, 4, 4, 2),
-                                               (64, 256, 4, 4, 1), (12, 3, 2, 8, 1)])
-def test_emulated_shards_match_oracle(world, n, m, k, ranks, split):
+                                               (64, 256, 4, 4, 1), (12, 3, 2, 8, 1), (2000, 16, 40, 16, 9),
+                                               (700, 32, 17, 4, 25)])
+def test_emulated_shards_match_oracle(world, n, m, k, ranks, split, fused, monkeypatch):
+    """fused: M <= 32 plans run Algorithm 1 as the two cooperative shard-tree kernels
+    (BTD_FUSED_TREE=0: per-level GEMM launches); both must match the oracle."""
     if (min(n, ranks * split)) % world:
         pytest.skip("ranges not divisible by world")
+    if not fused and m > 32:
+        pytest.skip("the fused shard tree only exists for M <= 32")
+    monkeypatch.setenv("BTD_FUSED_TREE", "1" if fused else "0")
     d, lo, up, f = configs.dominant_numpy(n, m, k, seed=n + world)
     res = _emulate(d, lo, up, f, ranks, split, world)
     assert res[0] == "ok"
