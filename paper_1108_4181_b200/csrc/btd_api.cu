@@ -424,6 +424,8 @@ struct btd_plan {
   int nz = 0;
   const int64_t *z_id = nullptr, *z_roff = nullptr, *z_rld = nullptr, *z_nlo = nullptr;
   SplitK z_split;
+  SplitK cross_split;              // crossing-node partial sums (sharded phase B)
+  std::vector<int64_t> cross_kh;   // their reduction lengths (host)
   std::vector<int64_t> z_k;  // reduction length per z entry (host)
   const int64_t* z_kd = nullptr;  // ... (device)
   bool r_uniform = false;         // inverse rows stored with the common stride r_ld
@@ -1085,6 +1087,7 @@ void build_splits(btd_plan& pl) {
   const int64_t tiles = std::max<int64_t>(1, (mp + 63) / 64);
   int64_t maxz = 0;
   pl.z_split = make_split(pl, pl.z_k, tiles, maxz);
+  pl.cross_split = make_split(pl, pl.cross_kh, tiles, maxz);
   for (auto& L_ : pl.levels) {
     std::vector<int64_t> kk(L_.count, mp);
     L_.split = make_split(pl, kk, tiles, maxz);
@@ -1334,6 +1337,7 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
     pl.ncross = (int)cn.size();
     pl.cross_node = pl.upload(cn); pl.cross_roff = pl.upload(cro); pl.cross_ld = pl.upload(cld);
     pl.cross_k = pl.upload(ck); pl.cross_lo = pl.upload(clo);
+    pl.cross_kh = ck;
     std::vector<int64_t> nlo(nn);
     for (int b = 0; b < nn; ++b) nlo[b] = pl.nodes[b].lo;
     pl.d_nlo = pl.upload(nlo);
@@ -1786,7 +1790,7 @@ void solve_shard_b(btd_plan& pl, const double* carry_all, double* partial_out, i
   launch_gemm(mp, K, pl.ncross, mk(partial_out, nullptr, 0, mpK, K), none(), 0.0,
               {term(mk(pl.Rrows.d(), pl.cross_roff, 0, 1, 0, pl.cross_ld), mk(ft, pl.cross_lo, 0, mpK, K), 0, 1.0,
                     pl.cross_k)},
-              st);
+              st, split_with(pl.cross_split, pl));
 }
 
 // Sharded phase C: crossing-node sums, tree levels, local recovery.
