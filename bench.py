@@ -185,6 +185,20 @@ class ClockSampler:
                 pass
             self._stop.wait(self.period)
 
+    def sample_now(self):
+        """One synchronous sample (called right after the timed steps are enqueued, while
+        the GPU runs them: regions shorter than the polling period still get one)."""
+        if self.nvml is None:
+            return
+        nv = self.nvml
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            self.samples.append((float(sm), float(mx), {k for k, b in self.bits.items() if r & b}))
+        except Exception:
+            pass
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
@@ -421,6 +435,7 @@ def run_b200(args):
         for _ in range(args.steps):
             solve()
         e1.record(stream)
+        clk.sample_now()
         e1.synchronize()
         launches = _native.launch_count() - lc0
         if dist:

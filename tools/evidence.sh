@@ -7,7 +7,7 @@ T=/tmp/ev
 OUT=gpurun_out/ev
 mkdir -p $T $OUT
 export BTD_GRAPHS=0   # ncu replays individual kernels; graphs off for the captures only
-for c in ${CONFIGS:-c1 c0 c2 c3 c4}; do
+for c in ${CONFIGS:-c1 c0 c2 c3 c4 c3dd}; do
   BTD_GRAPHS=1 timeout 600 python bench.py --config $c > $OUT/bench_$c.json 2> $T/bench_$c.err
   echo "bench $c rc=$?"
 done
@@ -24,6 +24,7 @@ for c in ${NCU_CONFIGS:-c1 c2 c4 c3}; do
   echo "ncu $c rc=$?"
   python tools/ncu_summary.py $T/prof_$c.ncu-rep > $OUT/ncu_full_$c.txt 2>&1
   python tools/launch_shares.py $OUT/launch_shares_$c.json $c:$T/launches_$c.csv:$T/plain_$c.log > /dev/null 2>&1
+  grep -E "btd::|Kernel Name" $T/launches_$c.csv | tail -n 400 > $OUT/launches_$c.csv
   cp $T/plain_$c.log $OUT/
 done
 du -sh $OUT
