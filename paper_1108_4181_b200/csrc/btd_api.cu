@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -425,6 +426,9 @@ struct btd_plan {
   const int64_t *z_id = nullptr, *z_roff = nullptr, *z_rld = nullptr, *z_nlo = nullptr;
   SplitK z_split;
   SplitK cross_split;              // crossing-node partial sums (sharded phase B)
+  // mode 1: split-K maps of the per-row-step GEMMs when a step's batch is under one wave
+  // (a sharded c3 rank owns 1-4 ranges: 32-128 output tiles), keyed by (entries, K)
+  std::map<std::pair<int, int64_t>, SplitK> step_splits;
   std::vector<int64_t> cross_kh;   // their reduction lengths (host)
   std::vector<int64_t> z_k;  // reduction length per z entry (host)
   const int64_t* z_kd = nullptr;  // ... (device)
@@ -1481,9 +1485,24 @@ void ensure_scratch(btd_plan& pl, int64_t K) {
   CK(cudaMemset(S.ft.p, 0, (size_t)pl.nr * mpK * sizeof(double)));
   if (pl.fused_tree || pl.fused_shard)
     S.tpartial.alloc((size_t)std::max({pl.tree_chunks, pl.shard_chunks, 1}) * pl.mp * K * sizeof(double));
-  if (pl.partial_elems_per_k) S.partial.alloc((size_t)pl.partial_elems_per_k * K * sizeof(double));
+  size_t pbytes = (size_t)pl.partial_elems_per_k * K * sizeof(double);
+  if (pl.mode == 1) {  // split-K maps for row steps whose batch is under one wave
+    for (const auto& st1 : pl.steps1)
+      for (int cnt : {st1.cnt, st1.nx, st1.nt}) {
+        const int64_t tiles = ((pl.m + 127) / 128) * ((K + 63) / 64);
+        if (cnt <= 0 || cnt * tiles >= 148 || pl.step_splits.count({cnt, K})) continue;
+        int64_t maxz = 0;
+        SplitK sp = make_split(pl, std::vector<int64_t>(cnt, pl.mp), tiles, maxz);
+        pl.step_splits[{cnt, K}] = sp;
+        pbytes = std::max(pbytes, (size_t)maxz * pl.m * K * sizeof(double));
+      }
+  }
+  if (pbytes) S.partial.alloc(pbytes);
   S.k = K;
 }
+
+
+const SplitK* step_split(btd_plan& pl, int cnt, int64_t K);
 
 ChainArgs chain_args(btd_plan& pl, const double* F, double* X, int64_t K, double* base, int64_t base_stride) {
   const int64_t blk = pl.blk;
@@ -1523,16 +1542,18 @@ void solve_forward(btd_plan& pl, const double* F, double* X, int64_t K, double* 
   for (int64_t j = 0; j < pl.cap; ++j) {
     const auto& s = pl.steps1[j];
     if (s.cnt == 0) break;
+    const SplitK* ssp = step_split(pl, s.cnt, K);  // few ranges (sharded): split the reductions
     if (j == 0)
       launch_gemm(m, K, s.cnt, mk(X, pl.d_lo, 1, mK, K), none(), 0.0,
-                  {term(mk(pool, pl.d_slot0, pl.off_Dinv, blk, mp), mk(F, pl.d_lo, 1, mK, K), m)}, st);
+                  {term(mk(pool, pl.d_slot0, pl.off_Dinv, blk, mp), mk(F, pl.d_lo, 1, mK, K), m)}, st, ssp);
     else
       launch_gemm(m, K, s.cnt, mk(X, pl.d_lo, 1 + j, mK, K), none(), 0.0,
                   {term(mk(pool, pl.d_slot0, pl.off_Dinv + j, blk, mp), mk(F, pl.d_lo, 1 + j, mK, K), m),
                    term(mk(pool, pl.d_slot0, pl.off_AD + j, blk, mp), mk(X, pl.d_lo, j, mK, K), m)},
-                  st);
+                  st, ssp);
     launch_gemm(mp, K, s.cnt, mk(base, nullptr, 0, base_stride, K), mk(base, nullptr, 0, base_stride, K), 1.0,
-                {term(mk(pool, pl.d_slot0, pl.off_Tb + j, blk, mp), mk(X, pl.d_lo, 1 + j, mK, K), m)}, st);
+                {term(mk(pool, pl.d_slot0, pl.off_Tb + j, blk, mp), mk(X, pl.d_lo, 1 + j, mK, K), m)}, st,
+                step_split(pl, s.cnt, K));
   }
 }
 
@@ -1551,6 +1572,13 @@ const SplitK* split_with(const SplitK& sp, btd_plan& pl) {
   tmp = sp;
   tmp.partial = pl.S().partial.d();
   return &tmp;
+}
+
+// split-K map for a mode-1 row-step GEMM of `cnt` entries (nullptr: plain launch)
+const SplitK* step_split(btd_plan& pl, int cnt, int64_t K) {
+  auto it = pl.step_splits.find({cnt, K});
+  if (it == pl.step_splits.end() || it->second.ntotal == 0) return nullptr;
+  return split_with(it->second, pl);
 }
 
 // Algorithm 1, level part: x~_k = z_node + E x~_{lo-1} + H x~_{hi+1}, level by level.
@@ -1655,12 +1683,12 @@ void solve_backward(btd_plan& pl, const double* F, double* X, int64_t K, cudaStr
     launch_gemm(m, K, s.nx, mk(X, s.x_row, 0, mK, K), mk(X, s.x_row, 0, mK, K), 1.0,
                 {term(mk(pool, s.x_slot, pl.off_G, blk, mp), mk(xt, s.x_q, 0, mpK, K), mp),
                  term(mk(pool, s.x_slot, pl.off_S, blk, mp), mk(X, s.x_row, 1, mK, K), m)},
-                st);
+                st, step_split(pl, s.nx, K));
     // last interior row: x_{j+1} = x~_{q+1}
     launch_gemm(m, K, s.nt, mk(X, s.t_row, 0, mK, K), mk(X, s.t_row, 0, mK, K), 1.0,
                 {term(mk(pool, s.t_slot, pl.off_G, blk, mp), mk(xt, s.t_q, 0, mpK, K), mp),
                  term(mk(pool, s.t_slot, pl.off_S, blk, mp), mk(xt, s.t_q, 1, mpK, K), mp)},
-                st);
+                st, step_split(pl, s.nt, K));
   }
 }
 
