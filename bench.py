@@ -69,7 +69,7 @@ def plan_params(name, world, ranks=0, split=0):
     """(ranks, split): split = the smallest second-level factor with at least
     ranges_per_gpu device ranges per GPU that are a whole multiple of it (the
     sweep grids are whole waves: c4 at 32 subdomains/GPU -> split 37, 1184
-    ranges, not split 19 -> 608 ranges = 4.1 waves; profiles/r01_ab_bwd.txt)."""
+    ranges, not split 19 -> 608 ranges = 4.1 waves; profiles/r01_chain_ab.txt)."""
     bc = BENCH_CFG[name]
     spg = bc["subdomains_per_gpu"](world)
     r = ranks or spg * world

@@ -240,7 +240,7 @@ BTD_DEVINL void group_sync(int wc) {
   }
 }
 
-template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1>
+template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1>
 struct ChainCfg {
   static constexpr int NW = WR * WC, NT = 32 * NW;
   static constexpr int RW = MP / WR, CW = KT / WC;
@@ -248,7 +248,7 @@ struct ChainCfg {
   static constexpr int LD = KT + 2;  // == 2 (mod 16) when KT % 16 == 0
   static constexpr int NS = MP / 8;  // pair steps per block product
   // factor-fragment prefetch distance (pair steps), one group ahead
-  static constexpr int PF = NS < 4 ? NS : (TM >= 4 ? 2 : 4);
+  static constexpr int PF = PF_ > 0 ? (PF_ < NS ? PF_ : NS) : (NS < 4 ? NS : (TM >= 4 ? 2 : 4));
   static constexpr int GPS = NS / PF;  // groups per segment
   // cp.async ring depths: forward F tiles, backward y tiles (0 = register prefetch)
   // (measured on B200: deeper rings hurt the 16x16 one-warp tiles of c4)
@@ -326,9 +326,9 @@ struct FragCursor {
 // Forward sweep.  Per interior row j, three segments stream through the same
 // register ring:  seg0 acc += AD_j y_{j-1};  seg1 ser += Tb_{j-1} y_{j-1};
 // seg2 acc += Dinv_j f_g.  (At j = 0, y_{-1} = 0 and seg1 reuses Tb_0.)
-template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1>
+template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1>
 __global__ void __launch_bounds__(32 * WR * WC) chain_fwd_kernel(ChainArgs a) {
-  using Cfg = ChainCfg<MP, KT, WR, WC, NF_, NY_>;
+  using Cfg = ChainCfg<MP, KT, WR, WC, NF_, NY_, PF_>;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, LD = Cfg::LD, NT = Cfg::NT, PF = Cfg::PF, GPS = Cfg::GPS;
   constexpr int NF = Cfg::NF;
   extern __shared__ __align__(16) double sm[];
@@ -446,9 +446,9 @@ BTD_DEVINL void load_smem(double (&acc)[TM][TN][2], const double* Ys, int ld, in
 
 // Backward sweep: per row j (descending) two segments through one ring:
 // seg0 acc += G_j x~_q ; seg1 acc += S_j x_{j+1}, with acc initialised to y_j.
-template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1>
+template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1>
 __global__ void __launch_bounds__(32 * WR * WC) chain_bwd_kernel(ChainArgs a) {
-  using Cfg = ChainCfg<MP, KT, WR, WC, NF_, NY_>;
+  using Cfg = ChainCfg<MP, KT, WR, WC, NF_, NY_, PF_>;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, LD = Cfg::LD, NT = Cfg::NT, PF = Cfg::PF, GPS = Cfg::GPS;
   constexpr int NY = Cfg::NY;
   extern __shared__ __align__(16) double sm[];
