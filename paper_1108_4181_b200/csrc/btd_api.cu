@@ -788,6 +788,10 @@ void launch_chain(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
       else if (variant == 11) launch_chain_t<256, 16, 16, 1, -1, -1, 2>(a, fwd, st);
       else if (variant == 12) launch_chain_t<256, 16, 16, 1, -1, -1, 8>(a, fwd, st);
       else if (variant == 13) launch_chain_t<256, 32, 32, 1, -1, -1, 1>(a, fwd, st);
+      else if (variant == 14) launch_chain_t<256, 16, 16, 1, 2, 3, 8>(a, fwd, st);
+      else if (variant == 15) launch_chain_t<256, 16, 16, 1, 2, 2, 8>(a, fwd, st);
+      else if (variant == 16) launch_chain_t<256, 32, 16, 1, 2, 0, 8>(a, fwd, st);
+      else if (variant == 17) launch_chain_t<256, 16, 16, 1, 2, 3, 4>(a, fwd, st);
       // measured (c1, profiles/r01_chain_ab.txt): forward factor fragments 8 pair steps ahead
       // (13.08 -> 12.74 ms; 2 ahead: 17.1 ms), 32-warp CTAs backward (-4%)
       else if (fwd) launch_chain_t<256, 16, 16, 1, -1, -1, 8>(a, fwd, st);
