@@ -52,8 +52,11 @@ BENCH_CFG = {
     # of waves (c1 fwd 37 x 16 tiles = 4 x 148 CTAs, bwd 37 x 8 = 2 x 148; c2 fwd 37 x 8 =
     # 2 x 148).  Measured on B200 (profiles/r01_ranks_sweep.txt): c1 P=36 0.848 -> P=37 0.868
     # of roofline, c2 0.785 -> 0.802; P=48 or 56 drops to 0.69-0.75 (partial last wave)
-    "c1": dict(subdomains_per_gpu=lambda w: 37, ranges_per_gpu=37),
-    "c2": dict(subdomains_per_gpu=lambda w: 37, ranges_per_gpu=37),
+    # On 4 and 8 GPUs 18 ranges per GPU: the sharded tree (series sums and crossing partials
+    # over P = 18 W ranges) costs less than the partial last wave of the sweeps (projected
+    # c1 8 GPUs 3.55 -> 3.38 ms, c2 3.51 -> 3.40 ms; profiles/r01_shard_projection.txt)
+    "c1": dict(subdomains_per_gpu=lambda w: 37 if w <= 2 else 18, ranges_per_gpu=lambda w: 37 if w <= 2 else 18),
+    "c2": dict(subdomains_per_gpu=lambda w: 37 if w <= 2 else 18, ranges_per_gpu=lambda w: 37 if w <= 2 else 18),
     # c3: the explicit interface Schur complement S (N=63, M=2048) of the 64-subdomain
     # Helmholtz DD; P = 9 ranges of 7 interface rows on one GPU (288 GEMM tiles fill the
     # 296 CTA slots), P = 8 (a multiple of 2/4/8) when sharded
@@ -76,6 +79,7 @@ def plan_params(name, world, ranks=0, split=0):
     if split:
         return r, split
     rpg = bc["ranges_per_gpu"]
+    rpg = rpg(world) if callable(rpg) else rpg
     if bc.get("one_wave"):
         return r, max(1, rpg // spg)
     sp = max(1, -(-rpg // spg))

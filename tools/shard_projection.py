@@ -30,9 +30,9 @@ def ev():
     return torch.cuda.Event(enable_timing=True)
 
 
-def project(name, world, split=0, reps=3):
+def project(name, world, split=0, reps=3, ranks=0):
     cfg = configs.CONFIGS[name]
-    ranks, sp = bench.plan_params(name, world, 0, split)
+    ranks, sp = bench.plan_params(name, world, ranks, split)
     d, lo, up, F = configs.generate(name, device="cuda")
     n, m, K = cfg["n"], cfg["m"], cfg["k"]
     be = NativeBackend(0)
@@ -90,11 +90,12 @@ if __name__ == "__main__":
     ap.add_argument("--worlds", type=int, nargs="+", default=[1, 2, 4, 8])
     ap.add_argument("--split", type=int, default=0)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--ranks-per-gpu", type=int, default=0)
     a = ap.parse_args()
     torch.cuda.set_device(0)
     base = None
     for w in a.worlds:
-        r = project(a.config, w, a.split, a.reps)
+        r = project(a.config, w, a.split, a.reps, a.ranks_per_gpu * w)
         base = base or (r["rhs_per_s"] if w == 1 else None)
         if base:
             r["projected_efficiency"] = r["rhs_per_s"] / (w * base)
