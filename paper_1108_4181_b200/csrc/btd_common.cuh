@@ -61,7 +61,13 @@ BTD_DEVINL void warp_prefetch_l2(const void* p, int64_t bytes, int lane) {
 
 // 16B read-only streaming load of a factor fragment (L2-resident factors,
 // re-read by the CTAs that share a range; keep them out of L1).
-BTD_DEVINL double2 ldg_cg2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
+#ifndef BTD_FRAG_NC
+#define BTD_FRAG_NC 0
+#endif
+BTD_DEVINL double2 ldg_cg2(const double* p) {
+  if constexpr (BTD_FRAG_NC) return __ldg(reinterpret_cast<const double2*>(p));  // L1-cached variant (A/B)
+  return __ldcg(reinterpret_cast<const double2*>(p));
+}
 
 // ---- mbarrier + bulk async copy (TMA engine, 1-D) ------------------------------
 BTD_DEVINL void mbar_init(uint64_t* bar, unsigned count) {
