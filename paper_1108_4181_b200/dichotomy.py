@@ -188,6 +188,8 @@ def _solve_tensor(plan, f):
     if f.dim() not in (2, 3) or f.shape[0] != plan.n or f.shape[1] != plan.m:
         raise _err.DimensionMismatch(
             f"rhs layout {tuple(f.shape[:2])} does not match plan ({plan.n}, {plan.m})")
+    if not squeeze and f.shape[2] == 0:
+        raise _err.empty_rhs("right-hand-side batch with zero columns")
     fk = f.unsqueeze(2) if squeeze else f
     fk = fk.to(device=f"cuda:{plan.device}", dtype=t.float64).contiguous()
     x = t.empty_like(fk)
@@ -218,7 +220,7 @@ def plan_solve(plan, f_batch):
     the device)."""
     if isinstance(f_batch, (list, tuple)):
         if not f_batch:
-            raise _err.DimensionMismatch("empty right-hand-side list")
+            raise _err.empty_rhs("empty right-hand-side list")
         cls = type(f_batch[0])
         stacked = np.stack([bv.data for bv in f_batch], axis=2)
         out = plan_solve(plan, stacked)
@@ -230,6 +232,8 @@ def plan_solve(plan, f_batch):
     if data.ndim not in (2, 3) or data.shape[0] != plan.n or data.shape[1] != plan.m:
         raise _err.DimensionMismatch(
             f"rhs layout {data.shape[:2]} does not match plan ({plan.n}, {plan.m})")
+    if data.ndim == 3 and data.shape[2] == 0:
+        raise _err.empty_rhs("right-hand-side batch with zero columns")
     x = _solve_host(plan, data)
     return type(f_batch)(x) if is_bv else x
 

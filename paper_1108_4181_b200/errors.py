@@ -104,3 +104,19 @@ def rebind(module) -> None:
 
 def get(name):
     return _BY_NAME[name]
+
+
+_EMPTY = {}
+
+
+def empty_rhs(message):
+    """Error for a zero-column batch or an empty list of right-hand sides.  The
+    reference fails there inside numpy with a ``ValueError`` (``np.stack`` of an
+    empty list, a reshape of a size-0 array; ref dichotomy.py:364-378); this one
+    is both the (current) ``DimensionMismatch`` and a ``ValueError`` so either
+    ``except`` clause keeps working."""
+    base = globals()["DimensionMismatch"]
+    cls = _EMPTY.get(base)
+    if cls is None:
+        cls = _EMPTY[base] = type("EmptyRightHandSide", (base, ValueError), {"__module__": __name__})
+    return cls(message)
