@@ -429,6 +429,7 @@ struct btd_plan {
   // mode 1: split-K maps of the per-row-step GEMMs when a step's batch is under one wave
   // (a sharded c3 rank owns 1-4 ranges: 32-128 output tiles), keyed by (entries, K)
   std::map<std::pair<int, int64_t>, SplitK> step_splits;
+  bool host_concurrent = false;  // host pipeline with >1 compute stream: chunks fill the GPU together
   std::vector<int64_t> cross_kh;   // their reduction lengths (host)
   std::vector<int64_t> z_k;  // reduction length per z entry (host)
   const int64_t* z_kd = nullptr;  // ... (device)
@@ -1505,11 +1506,14 @@ void ensure_scratch(btd_plan& pl, int64_t K) {
     for (const auto& st1 : pl.steps1)
       for (int cnt : {st1.cnt, st1.nx, st1.nt}) {
         const int64_t tiles = ((pl.m + 127) / 128) * ((K + 63) / 64);
-        if (cnt <= 0 || cnt * tiles >= 148 || pl.step_splits.count({cnt, K})) continue;
-        int64_t maxz = 0;
-        SplitK sp = make_split(pl, std::vector<int64_t>(cnt, pl.mp), tiles, maxz);
-        pl.step_splits[{cnt, K}] = sp;
-        pbytes = std::max(pbytes, (size_t)maxz * pl.m * K * sizeof(double));
+        if (cnt <= 0 || cnt * tiles >= 148) continue;
+        auto it = pl.step_splits.find({cnt, K});
+        if (it == pl.step_splits.end()) {  // (maps are per plan; the partials buffer is per slot)
+          int64_t maxz = 0;
+          it = pl.step_splits.emplace(std::make_pair(cnt, K),
+                                      make_split(pl, std::vector<int64_t>(cnt, pl.mp), tiles, maxz)).first;
+        }
+        pbytes = std::max(pbytes, (size_t)it->second.ntotal * pl.mp * K * sizeof(double));
       }
   }
   if (pbytes) S.partial.alloc(pbytes);
@@ -1591,6 +1595,7 @@ const SplitK* split_with(const SplitK& sp, btd_plan& pl) {
 
 // split-K map for a mode-1 row-step GEMM of `cnt` entries (nullptr: plain launch)
 const SplitK* step_split(btd_plan& pl, int cnt, int64_t K) {
+  if (pl.host_concurrent) return nullptr;  // concurrent chunk solves already fill the GPU
   auto it = pl.step_splits.find({cnt, K});
   if (it == pl.step_splits.end() || it->second.ntotal == 0) return nullptr;
   return split_with(it->second, pl);
@@ -2162,8 +2167,9 @@ int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int6
     }
     struct SlotReset {
       btd_plan* p;
-      ~SlotReset() { p->cur = 0; }
+      ~SlotReset() { p->cur = 0; p->host_concurrent = false; }
     } reset{pl};
+    pl->host_concurrent = nstr > 1;
     for (int sl = 0; sl < nstr; ++sl) {
       pl->cur = sl;
       ensure_scratch(*pl, kc);

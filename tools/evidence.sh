@@ -17,9 +17,9 @@ for c in ${NCU_CONFIGS:-c1 c2 c4 c3}; do
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $T/launches_$c.csv $CMD > /dev/null 2>&1
   if [ $c = c3 ]; then
     n=$(grep -c "gemm_tma_kernel" $T/launches_$c.csv); skip=$((n - 12))
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tma -s $skip -c 2 -o $T/prof_$c $CMD > $T/ncu_$c.log 2>&1
+    timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:gemm_tma -s $skip -c 2 -o $T/prof_$c $CMD > $T/ncu_$c.log 2>&1
   else
-    timeout 900 ncu --set full --clock-control none --import-source on -k "regex:chain_|stream_" -s 2 -c 2 -o $T/prof_$c $CMD > $T/ncu_$c.log 2>&1
+    timeout 900 ncu -f --set full --clock-control none --import-source on -k "regex:chain_|stream_" -s 2 -c 2 -o $T/prof_$c $CMD > $T/ncu_$c.log 2>&1
   fi
   echo "ncu $c rc=$?"
   python tools/ncu_summary.py $T/prof_$c.ncu-rep > $OUT/ncu_full_$c.txt 2>&1
