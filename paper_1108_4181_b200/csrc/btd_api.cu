@@ -670,18 +670,18 @@ void launch_inv(btd_plan& pl, int nbatch, const double* in, const int64_t* idx_i
 }
 
 // ---------------------------------------------------------------- chain kernels
-template <int MP, int KT, int WR, int WC, int NF = -1, int NY = -1, int PF = -1>
+template <int MP, int KT, int WR, int WC, int NF = -1, int NY = -1, int PF = -1, int MINB = 1>
 void launch_chain_t(const ChainArgs& a, bool fwd, cudaStream_t st) {
   using Cfg = ChainCfg<MP, KT, WR, WC, NF, NY, PF>;
   const size_t smem = (size_t)(fwd ? Cfg::FWD_BUFS : Cfg::BWD_BUFS) * MP * Cfg::LD * sizeof(double);
   const int64_t ntile = (a.K + KT - 1) / KT;
   dim3 grid((unsigned)ntile, (unsigned)a.nr);
   if (fwd) {
-    set_smem_attr((const void*)chain_fwd_kernel<MP, KT, WR, WC, NF, NY, PF>, smem);
-    chain_fwd_kernel<MP, KT, WR, WC, NF, NY, PF><<<grid, Cfg::NT, smem, st>>>(a);
+    set_smem_attr((const void*)chain_fwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB>, smem);
+    chain_fwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB><<<grid, Cfg::NT, smem, st>>>(a);
   } else {
-    set_smem_attr((const void*)chain_bwd_kernel<MP, KT, WR, WC, NF, NY, PF>, smem);
-    chain_bwd_kernel<MP, KT, WR, WC, NF, NY, PF><<<grid, Cfg::NT, smem, st>>>(a);
+    set_smem_attr((const void*)chain_bwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB>, smem);
+    chain_bwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB><<<grid, Cfg::NT, smem, st>>>(a);
   }
   CK_LAUNCH();
 }

@@ -326,8 +326,8 @@ struct FragCursor {
 // Forward sweep.  Per interior row j, three segments stream through the same
 // register ring:  seg0 acc += AD_j y_{j-1};  seg1 ser += Tb_{j-1} y_{j-1};
 // seg2 acc += Dinv_j f_g.  (At j = 0, y_{-1} = 0 and seg1 reuses Tb_0.)
-template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1>
-__global__ void __launch_bounds__(32 * WR * WC) chain_fwd_kernel(ChainArgs a) {
+template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1, int MINB_ = 1>
+__global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_fwd_kernel(ChainArgs a) {
   using Cfg = ChainCfg<MP, KT, WR, WC, NF_, NY_, PF_>;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, LD = Cfg::LD, NT = Cfg::NT, PF = Cfg::PF, GPS = Cfg::GPS;
   constexpr int NF = Cfg::NF;
@@ -446,8 +446,8 @@ BTD_DEVINL void load_smem(double (&acc)[TM][TN][2], const double* Ys, int ld, in
 
 // Backward sweep: per row j (descending) two segments through one ring:
 // seg0 acc += G_j x~_q ; seg1 acc += S_j x_{j+1}, with acc initialised to y_j.
-template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1>
-__global__ void __launch_bounds__(32 * WR * WC) chain_bwd_kernel(ChainArgs a) {
+template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1, int MINB_ = 1>
+__global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_bwd_kernel(ChainArgs a) {
   using Cfg = ChainCfg<MP, KT, WR, WC, NF_, NY_, PF_>;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, LD = Cfg::LD, NT = Cfg::NT, PF = Cfg::PF, GPS = Cfg::GPS;
   constexpr int NY = Cfg::NY;
