@@ -550,7 +550,12 @@ def run_b200(args):
                    "l2": "inputs larger than L2 (F %.2f GB, factors %.2f GB per GPU)" % (
                        F.numel() * 8 / 1e9, fbytes / 1e9)},
         "roofline": roof,
-        "solve_roofline": {"flops_per_gpu": tot_flops, "bytes_per_gpu": tot_bytes, "t_roof_ms": t_roof * 1e3,
+        "solve_roofline": {"flops_per_gpu": tot_flops, "bytes_per_gpu": tot_bytes,
+                           # SURVEY 8(d) companions: strict lower bound 8(5M^2 + 2MK) and the
+                           # reference pipeline's 8(5M^2 + 6MK) bytes per block row
+                           "bytes_strict_per_gpu": 8.0 * (5 * m * m + 2 * m * K) * n / world,
+                           "bytes_ref_pipeline_per_gpu": 8.0 * (5 * m * m + 6 * m * K) * n / world,
+                           "t_roof_ms": t_roof * 1e3,
                            "frac": t_roof * 1e3 / ms_step, "fp64_tflops_peak": fp64, "hbm_gbs_peak": hbm},
         "phases_ms": {"forward": ph[0], "interface_tree": ph[1], "backward": ph[2], "total": ph[3]},
         "plan_build_s": build_s,
