@@ -482,6 +482,8 @@ struct btd_plan {
     DevBuf ft, zbuf, xt, partial, tpartial, fcopy;
     cudaStream_t own = nullptr;  // graph replay stream
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    cudaStream_t side = nullptr;  // mode 1: base-accumulation GEMMs beside the row steps
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   };
   static constexpr int kSlots = 4;  // host pipeline: chunk c solves in slot c % nstreams
   Scratch sc[kSlots];
@@ -551,6 +553,9 @@ struct btd_plan {
       if (x.own) cudaStreamDestroy(x.own);
       if (x.ev_in) cudaEventDestroy(x.ev_in);
       if (x.ev_out) cudaEventDestroy(x.ev_out);
+      if (x.side) cudaStreamDestroy(x.side);
+      if (x.ev_fork) cudaEventDestroy(x.ev_fork);
+      if (x.ev_join) cudaEventDestroy(x.ev_join);
     }
     if (s_in) cudaStreamDestroy(s_in);
     if (s_out) cudaStreamDestroy(s_out);
@@ -1556,8 +1561,19 @@ void solve_forward(btd_plan& pl, const double* F, double* X, int64_t K, double* 
     CK(cudaMemcpyAsync(fc.p, F, fbytes, cudaMemcpyDeviceToDevice, st));
     F = fc.d();
   }
-  // mode 1: base_q = F[lo_q] (rows < m; pad rows stay 0), then one GEMM launch per row step
+  // mode 1: base_q = F[lo_q] (rows < m; pad rows stay 0), then one GEMM launch per row step.
+  // base += Tb_j y_j only reads y_j, like row j+1's product: without split-K (whose partials
+  // buffer is shared) it runs on a side stream beside the next row step, so the two
+  // launches' CTAs pack into fewer waves (joined before the interface RHS).
   launch_gemm(m, K, pl.nlive, mk(base, nullptr, 0, base_stride, K), mk(F, pl.d_lo, 0, mK, K), 1.0, {}, st);
+  auto& S = pl.S();
+  const bool fork = pl.cap > 1 && pl.steps1[0].cnt > 0 && !step_split(pl, pl.steps1[0].cnt, K);
+  if (fork && !S.side) {
+    CK(cudaStreamCreateWithFlags(&S.side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&S.ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&S.ev_join, cudaEventDisableTiming));
+  }
+  bool forked = false;
   for (int64_t j = 0; j < pl.cap; ++j) {
     const auto& s = pl.steps1[j];
     if (s.cnt == 0) break;
@@ -1570,9 +1586,20 @@ void solve_forward(btd_plan& pl, const double* F, double* X, int64_t K, double* 
                   {term(mk(pool, pl.d_slot0, pl.off_Dinv + j, blk, mp), mk(F, pl.d_lo, 1 + j, mK, K), m),
                    term(mk(pool, pl.d_slot0, pl.off_AD + j, blk, mp), mk(X, pl.d_lo, j, mK, K), m)},
                   st, ssp);
+    cudaStream_t tst = st;
+    if (fork && !ssp) {
+      CK(cudaEventRecord(S.ev_fork, st));
+      CK(cudaStreamWaitEvent(S.side, S.ev_fork, 0));
+      tst = S.side;
+      forked = true;
+    }
     launch_gemm(mp, K, s.cnt, mk(base, nullptr, 0, base_stride, K), mk(base, nullptr, 0, base_stride, K), 1.0,
-                {term(mk(pool, pl.d_slot0, pl.off_Tb + j, blk, mp), mk(X, pl.d_lo, 1 + j, mK, K), m)}, st,
-                step_split(pl, s.cnt, K));
+                {term(mk(pool, pl.d_slot0, pl.off_Tb + j, blk, mp), mk(X, pl.d_lo, 1 + j, mK, K), m)}, tst,
+                ssp);
+  }
+  if (forked) {
+    CK(cudaEventRecord(S.ev_join, S.side));
+    CK(cudaStreamWaitEvent(st, S.ev_join, 0));
   }
 }
 
