@@ -47,7 +47,9 @@ sys.path.insert(0, ROOT)
 # per range and column tile fills the 148 SMs).  c4 follows the paired
 # reading of BASELINE.json: 8 / 16 / 32 / 64 subdomains per GPU on 1 / 2 / 4 / 8 GPUs.
 BENCH_CFG = {
-    "c0": dict(subdomains_per_gpu=lambda w: 4, ranges_per_gpu=4),
+    # c0: the reference's P = 4 subdomains, each split into 16 device ranges (chains of 8 rows:
+    # the solve is latency-bound; split 1 -> 16: 0.152 -> 0.049 ms per step, profiles/r01_chain_ab.txt)
+    "c0": dict(subdomains_per_gpu=lambda w: 4, ranges_per_gpu=64),
     # c1/c2: 37 ranges per GPU (148 = 4 x 37): every chain kernel's grid is a whole number
     # of waves (c1 fwd 37 x 16 tiles = 4 x 148 CTAs, bwd 37 x 8 = 2 x 148; c2 fwd 37 x 8 =
     # 2 x 148).  Measured on B200 (profiles/r01_ranks_sweep.txt): c1 P=36 0.848 -> P=37 0.868
