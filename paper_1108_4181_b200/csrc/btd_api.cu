@@ -2154,7 +2154,9 @@ int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int6
       const char* e = getenv("BTD_HOST_MINW");
       minw_env = e ? std::max(2, atoi(e)) : 0;
     }
-    const int64_t minw = minw_env ? minw_env : (k >= 256 ? 64 : 32);
+    // mode 1 (blocks > 256): the solve outweighs the copies; narrow chunks only thin out its
+    // GEMM batches (c3: 32-column chunks 8.2k, one 128-column chunk 8.4k RHS/s end to end)
+    const int64_t minw = minw_env ? minw_env : (pl->mode == 1 ? 128 : (k >= 256 ? 64 : 32));
     int64_t kc = k;
     for (int64_t nch = maxch; nch >= 2; --nch)
       if (k % nch == 0 && (k / nch) % 2 == 0 && k / nch >= minw) { kc = k / nch; break; }
