@@ -1592,6 +1592,10 @@ void solve_forward(btd_plan& pl, const double* F, double* X, int64_t K, double* 
       CK(cudaStreamWaitEvent(S.side, S.ev_fork, 0));
       tst = S.side;
       forked = true;
+    } else if (forked) {  // a split step (ragged ranges): finish the side's base updates first
+      CK(cudaEventRecord(S.ev_join, S.side));
+      CK(cudaStreamWaitEvent(st, S.ev_join, 0));
+      forked = false;
     }
     launch_gemm(mp, K, s.cnt, mk(base, nullptr, 0, base_stride, K), mk(base, nullptr, 0, base_stride, K), 1.0,
                 {term(mk(pool, pl.d_slot0, pl.off_Tb + j, blk, mp), mk(X, pl.d_lo, 1 + j, mK, K), m)}, tst,
