@@ -213,7 +213,8 @@ def test_large_blocks_tma_gemm_paths(n, m, k, ranks, split, mode, monkeypatch):
     _check(d, lo, up, x, f, ref)
 
 
-@pytest.mark.parametrize("n,m,k,ranks", [(24, 384, 16, 3), (30, 320, 64, 2), (40, 512, 96, 4)])
+@pytest.mark.parametrize("n,m,k,ranks", [(24, 384, 16, 3), (30, 320, 64, 2), (40, 512, 96, 4),
+                                         (149, 384, 64, 52)])  # ragged: step 0 unsplit (50 ranges), step 1 split
 def test_mode1_split_row_steps_device_and_host_pipeline(n, m, k, ranks, monkeypatch):
     """Mode-1 row steps whose batch is under one wave run split-K (maps keyed by batch
     size and K); the host pipeline solves narrower column chunks on up to four
