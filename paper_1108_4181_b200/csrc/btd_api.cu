@@ -600,8 +600,12 @@ void launch_inv(btd_plan& pl, int nbatch, const double* in, const int64_t* idx_i
     // diag(U), getrs(transpose) against I -> D^{-1} written row-major.
     auto host_idx = [&](const int64_t* di) {
       std::vector<int64_t> h(nbatch);
-      if (di) CK(cudaMemcpy(h.data(), di, sizeof(int64_t) * nbatch, cudaMemcpyDeviceToHost));
-      else for (int b = 0; b < nbatch; ++b) h[b] = b;
+      if (di) {  // stream-ordered: the index arrays may still be in flight on st (StagedUploads)
+        CK(cudaMemcpyAsync(h.data(), di, sizeof(int64_t) * nbatch, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      } else {
+        for (int b = 0; b < nbatch; ++b) h[b] = b;
+      }
       return h;
     };
     const std::vector<int64_t> hin = host_idx(idx_in), hout = host_idx(idx_out), hmap = host_idx(fail_map);
@@ -728,7 +732,25 @@ bool launch_stream(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
 
 // Chain-kernel configuration per padded block order (MP, KT, warp rows x warp cols).
 // BTD_CHAIN_VARIANT selects alternatives for tuning experiments.
+void launch_chain_slice(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st);
+
+// Sweep kernels index ranges by blockIdx.y (at most 65535): more ranges (ranks * split up to
+// N) run as consecutive slices with the per-range arrays and outputs offset.
 void launch_chain(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
+  constexpr int kMaxY = 65535;
+  for (int q0 = 0; q0 < a.nr; q0 += kMaxY) {
+    ChainArgs s = a;
+    s.nr = std::min(kMaxY, a.nr - q0);
+    s.lo = a.lo + q0;
+    s.nint = a.nint + q0;
+    s.slot0 = a.slot0 + q0;
+    if (a.base) s.base = a.base + (int64_t)q0 * a.base_stride;
+    if (a.xt) s.xt = a.xt + (int64_t)q0 * mp * a.K;
+    launch_chain_slice(mp, s, fwd, st);
+  }
+}
+
+void launch_chain_slice(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
   if (a.nr <= 0) return;
   if (launch_stream(mp, a, fwd, st)) return;
   static int variant_f = -1, variant_b = -1;
@@ -1120,6 +1142,49 @@ void build_splits(btd_plan& pl) {
   pl.partial_elems_per_k = maxz * mp;
 }
 
+// Index arrays for the many small launches of the tree build, sub-allocated from 4 MB pinned +
+// device chunks and copied with cudaMemcpyAsync on the build stream.  (A cudaMalloc plus a
+// blocking cudaMemcpy per array made plans of 20000 device ranges take ~20 s: the root's
+// inverse rows are a sequential sweep over all ranges, a few launches per step.)
+class StagedUploads {
+ public:
+  explicit StagedUploads(cudaStream_t st) : st_(st) {}
+  StagedUploads(const StagedUploads&) = delete;
+  StagedUploads& operator=(const StagedUploads&) = delete;
+  ~StagedUploads() {
+    cudaStreamSynchronize(st_);  // copies and the kernels reading them are done
+    for (void* p : host_) cudaFreeHost(p);
+    for (void* p : dev_) cudaFree(p);
+  }
+  template <class T>
+  const T* put(const std::vector<T>& v) {
+    const size_t bytes = (std::max<size_t>(v.size() * sizeof(T), 16) + 15) / 16 * 16;
+    if (host_.empty() || off_ + bytes > cap_) {
+      cap_ = std::max<size_t>(kChunk, bytes);
+      void *h = nullptr, *d = nullptr;
+      CK(cudaMallocHost(&h, cap_));
+      host_.push_back(h);
+      CK(cudaMalloc(&d, cap_));
+      dev_.push_back(d);
+      off_ = 0;
+    }
+    char* h = static_cast<char*>(host_.back()) + off_;
+    char* d = static_cast<char*>(dev_.back()) + off_;
+    if (!v.empty()) {
+      memcpy(h, v.data(), v.size() * sizeof(T));
+      CK(cudaMemcpyAsync(d, h, v.size() * sizeof(T), cudaMemcpyHostToDevice, st_));
+    }
+    off_ += bytes;
+    return reinterpret_cast<const T*>(d);
+  }
+
+ private:
+  static constexpr size_t kChunk = size_t(4) << 20;
+  cudaStream_t st_;
+  std::vector<void*> host_, dev_;
+  size_t off_ = 0, cap_ = 0;
+};
+
 // ---------------------------------------------------------------- plan build, global part
 // contrib_all: [nr][4][mp][mp] device, identical on every rank.
 void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int64_t* err_row, bool restore = false) {
@@ -1198,6 +1263,7 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
   tfc.alloc(sizeof(int32_t) * nn);
   CK(cudaMemsetAsync(tfs.p, 0xff, sizeof(int32_t) * nn, st));
   T = tp.d();
+  StagedUploads stg(st);
   for (int64_t lev = 0; lev <= maxlevel; ++lev) {
     std::vector<int> ids;
     int64_t smax = 0;
@@ -1224,18 +1290,18 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
       }
       const int cnt = (int)dt_c.size();
       if (i == 0)
-        launch_gemm(mp, mp, cnt, mk(T, pl.upload(dt_c), 0, blk, mp), mk(pool, pl.upload(dt_in), 0, blk, mp), 1.0, {}, st);
+        launch_gemm(mp, mp, cnt, mk(T, stg.put(dt_c), 0, blk, mp), mk(pool, stg.put(dt_in), 0, blk, mp), 1.0, {}, st);
       else
-        launch_gemm(mp, mp, cnt, mk(T, pl.upload(dt_c), 0, blk, mp), mk(pool, pl.upload(dt_in), 0, blk, mp), 1.0,
-                    {term(mk(pool, pl.upload(dt_a), 0, blk, mp), mk(T, pl.upload(dt_b), 0, blk, mp), mp, -1.0)}, st);
-      launch_inv(pl, cnt, T, pl.upload(inv_in), 0, T, pl.upload(inv_out), 0, (int)i, tfs.i32(), tfc.i32(), ws, st,
-                 pl.upload(failidx));
+        launch_gemm(mp, mp, cnt, mk(T, stg.put(dt_c), 0, blk, mp), mk(pool, stg.put(dt_in), 0, blk, mp), 1.0,
+                    {term(mk(pool, stg.put(dt_a), 0, blk, mp), mk(T, stg.put(dt_b), 0, blk, mp), mp, -1.0)}, st);
+      launch_inv(pl, cnt, T, stg.put(inv_in), 0, T, stg.put(inv_out), 0, (int)i, tfs.i32(), tfc.i32(), ws, st,
+                 stg.put(failidx));
       if (!sc.empty())
-        launch_gemm(mp, mp, (int)sc.size(), mk(T, pl.upload(sc), 0, blk, mp), none(), 0.0,
-                    {term(mk(T, pl.upload(sa), 0, blk, mp), mk(pool, pl.upload(sb), 0, blk, mp), mp)}, st);
+        launch_gemm(mp, mp, (int)sc.size(), mk(T, stg.put(sc), 0, blk, mp), none(), 0.0,
+                    {term(mk(T, stg.put(sa), 0, blk, mp), mk(pool, stg.put(sb), 0, blk, mp), mp)}, st);
       if (!ac.empty())
-        launch_gemm(mp, mp, (int)ac.size(), mk(T, pl.upload(ac), 0, blk, mp), none(), 0.0,
-                    {term(mk(T, pl.upload(aa), 0, blk, mp), mk(pool, pl.upload(ab), 0, blk, mp), mp)}, st);
+        launch_gemm(mp, mp, (int)ac.size(), mk(T, stg.put(ac), 0, blk, mp), none(), 0.0,
+                    {term(mk(T, stg.put(aa), 0, blk, mp), mk(pool, stg.put(ab), 0, blk, mp), mp)}, st);
     }
     // forward solve with unit RHS at kk = k - lo: y_kk = D'^{-1}_kk ; y_i = AD'_i y_{i-1}
     for (int64_t i = 0; i < smax; ++i) {
@@ -1247,10 +1313,10 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
         else if (i > kk) { gc.push_back(tpY + nb0[b] + i); ga.push_back(tpAD + nb0[b] + i); gb.push_back(tpY + nb0[b] + i - 1); }
       }
       if (!cc.empty())
-        launch_gemm(mp, mp, (int)cc.size(), mk(T, pl.upload(cc), 0, blk, mp), mk(T, pl.upload(ci), 0, blk, mp), 1.0, {}, st);
+        launch_gemm(mp, mp, (int)cc.size(), mk(T, stg.put(cc), 0, blk, mp), mk(T, stg.put(ci), 0, blk, mp), 1.0, {}, st);
       if (!gc.empty())
-        launch_gemm(mp, mp, (int)gc.size(), mk(T, pl.upload(gc), 0, blk, mp), none(), 0.0,
-                    {term(mk(T, pl.upload(ga), 0, blk, mp), mk(T, pl.upload(gb), 0, blk, mp), mp)}, st);
+        launch_gemm(mp, mp, (int)gc.size(), mk(T, stg.put(gc), 0, blk, mp), none(), 0.0,
+                    {term(mk(T, stg.put(ga), 0, blk, mp), mk(T, stg.put(gb), 0, blk, mp), mp)}, st);
     }
     // backward: y_i += S'_i y_{i+1}
     for (int64_t i = smax - 2; i >= 0; --i) {
@@ -1260,9 +1326,9 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
         c.push_back(tpY + nb0[b] + i); a.push_back(tpS + nb0[b] + i); bb.push_back(tpY + nb0[b] + i + 1);
       }
       if (!c.empty()) {
-        const int64_t* dc = pl.upload(c);
+        const int64_t* dc = stg.put(c);
         launch_gemm(mp, mp, (int)c.size(), mk(T, dc, 0, blk, mp), mk(T, dc, 0, blk, mp), 1.0,
-                    {term(mk(T, pl.upload(a), 0, blk, mp), mk(T, pl.upload(bb), 0, blk, mp), mp)}, st);
+                    {term(mk(T, stg.put(a), 0, blk, mp), mk(T, stg.put(bb), 0, blk, mp), mp)}, st);
       }
     }
   }

@@ -214,7 +214,7 @@ def test_large_blocks_tma_gemm_paths(n, m, k, ranks, split, mode, monkeypatch):
 
 
 @pytest.mark.parametrize("n,m,k,ranks", [(24, 384, 16, 3), (30, 320, 64, 2), (40, 512, 96, 4),
-                                         (149, 384, 64, 52)])  # ragged: step 0 unsplit (50 ranges), step 1 split
+                                         (443, 128, 64, 150)])  # ragged: step 0 unsplit (148 ranges), step 1 split
 def test_mode1_split_row_steps_device_and_host_pipeline(n, m, k, ranks, monkeypatch):
     """Mode-1 row steps whose batch is under one wave run split-K (maps keyed by batch
     size and K); the host pipeline solves narrower column chunks on up to four
@@ -230,3 +230,19 @@ def test_mode1_split_row_steps_device_and_host_pipeline(n, m, k, ranks, monkeypa
     for _ in range(3):  # repeated host solves replay per-slot graphs
         x_host = plan_solve(plan, f)
         _check(d, lo, up, x_host, f, ref)
+
+
+@pytest.mark.parametrize("m,k", [(2, 3)])
+def test_more_device_ranges_than_grid_y(m, k):
+    """ranks * split above 65535 device ranges: the sweep kernels run in slices of 65535
+    ranges (blockIdx.y) with offset per-range arrays and outputs."""
+    import coracle
+
+    n, ranks, split = 160000, 4, 20000   # 80000 device ranges of 2 rows
+    d, lo, up, f = configs.dominant_numpy(n, m, k, seed=m + k)
+    plan = plan_build(BlockTriMatrix(d, lo, up), ranks, split=split)
+    assert plan.nranges > 65535
+    x = plan_solve(plan, f)
+    ref = coracle.CPlan(d, lo, up, ranks).solve(f)
+    assert O.max_rel_err(x, ref) <= 1e-9
+    assert O.rel_residual(d, lo, up, x, f) <= 1e-10
