@@ -176,7 +176,9 @@ int btd_plan_phase_times(btd_plan* plan, double* ms_out, int64_t* nsolves, int r
  * device chunk, stream-ordered (cudaMemcpy2DAsync; the per-rank host pipeline
  * of the sharded solve, ShardedPlan.solve_host).  to_device = 1: host columns
  * [c0, c0+kc) -> device; 0: device -> host columns.  Host memory should be
- * pinned to overlap with compute. */
+ * pinned to overlap with compute.  (The reference ranks exchange and solve on
+ * numpy arrays in host memory, harness.py:147-216; this moves a rank's rows
+ * in column chunks so the copies overlap its solve.) */
 int btd_copy_columns(double* host, int64_t rows, int64_t K, int64_t c0, int64_t kc, double* dev, int to_device,
                      void* stream);
 
