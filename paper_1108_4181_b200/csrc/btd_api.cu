@@ -361,8 +361,11 @@ void launch_gemm(int64_t rows, int64_t cols, int nbatch, Opnd C, Opnd Cin, doubl
   }
   CK_LAUNCH();
   if (d.split_b) {
+    // enough CTAs to fill the GPU even for one or two entries (c1/c3 tree levels: 64 x 1-2
+    // CTAs took 18-35 us per reduction)
     const int64_t per = rows * cols;
-    dim3 grid((unsigned)std::min<int64_t>((per + 255) / 256, 64), (unsigned)std::min(nbatch, 65535));
+    const int64_t bx = std::max<int64_t>(64, 1184 / std::max(nbatch, 1));
+    dim3 grid((unsigned)std::min<int64_t>((per + 255) / 256, bx), (unsigned)std::min(nbatch, 65535));
     splitk_reduce_kernel<<<grid, 256, 0, st>>>(sp->partial, sp->zoff, sp->zcnt, C, Cin, beta, rows, cols, nbatch);
     CK_LAUNCH();
   }
