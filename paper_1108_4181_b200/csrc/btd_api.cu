@@ -444,6 +444,7 @@ struct btd_plan {
                   *h_idx = nullptr, *xh_idx = nullptr;
     const int64_t *e_k = nullptr, *h_k = nullptr;  // 0 where the correction block is zero
     SplitK split;
+    bool copy_only = false;  // no node of the level has a correction (the root): x~_k = z
   };
   int64_t partial_elems_per_k = 0;  // split-K scratch: doubles per unit K
   DevBuf partial;
@@ -1452,6 +1453,8 @@ void build_finish(btd_plan& pl, const double* contrib_all, cudaStream_t st, int6
       L_.c_idx = pl.upload(c); L_.z_idx = pl.upload(z); L_.e_idx = pl.upload(e);
       L_.xl_idx = pl.upload(xl); L_.h_idx = pl.upload(h); L_.xh_idx = pl.upload(xh);
       L_.e_k = pl.upload(ek); L_.h_k = pl.upload(hk);
+      L_.copy_only = std::all_of(ek.begin(), ek.end(), [](int64_t v) { return v == 0; }) &&
+                     std::all_of(hk.begin(), hk.end(), [](int64_t v) { return v == 0; });
     }
     // split-K plans: enough CTAs (>= 2 waves) for the series sums and the level corrections
     pl.z_k.clear();
@@ -1701,16 +1704,35 @@ const SplitK* step_split(btd_plan& pl, int cnt, int64_t K) {
   return split_with(it->second, pl);
 }
 
+// dst[dst_idx[b]] = src[src_idx[b]], blocks of `per` doubles
+__global__ void copy_blocks_kernel(double* dst, const int64_t* dst_idx, const double* src, const int64_t* src_idx,
+                                   int count, int64_t per) {
+  for (int b = blockIdx.y; b < count; b += gridDim.y) {
+    double* d = dst + dst_idx[b] * per;
+    const double* sp = src + src_idx[b] * per;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per; e += (int64_t)gridDim.x * blockDim.x)
+      d[e] = sp[e];
+  }
+}
+
 // Algorithm 1, level part: x~_k = z_node + E x~_{lo-1} + H x~_{hi+1}, level by level.
 void solve_levels(btd_plan& pl, int64_t K, cudaStream_t st) {
   const int64_t mp = pl.mp, blk = pl.blk, mpK = mp * K;
   double* xt = pl.S().xt.d();
   double* z = pl.S().zbuf.d();
-  for (const auto& lev : pl.levels)
+  for (const auto& lev : pl.levels) {
+    if (lev.count <= 0) continue;
+    if (lev.copy_only) {  // the root level: x~_k = z_root, a copy, not a GEMM + split-K reduction
+      dim3 grid((unsigned)std::min<int64_t>((mpK + 255) / 256, 592), (unsigned)std::min(lev.count, 65535));
+      copy_blocks_kernel<<<grid, 256, 0, st>>>(xt, lev.c_idx, z, lev.z_idx, lev.count, mpK);
+      CK_LAUNCH();
+      continue;
+    }
     launch_gemm(mp, K, lev.count, mk(xt, lev.c_idx, 0, mpK, K), mk(z, lev.z_idx, 0, mpK, K), 1.0,
                 {term(mk(pl.EH.d(), lev.e_idx, 0, blk, mp), mk(xt, lev.xl_idx, 0, mpK, K), mp, 1.0, lev.e_k),
                  term(mk(pl.EH.d(), lev.h_idx, 0, blk, mp), mk(xt, lev.xh_idx, 0, mpK, K), mp, 1.0, lev.h_k)},
                 st, split_with(lev.split, pl));
+  }
 }
 
 template <int MP>
