@@ -241,7 +241,7 @@ class ShardedPlan:
         self.be.solve_c(self.h, part_all, f_local, x_local, k)
         return x_local
 
-    def solve_host(self, f_host, x_host, chunks=4):
+    def solve_host(self, f_host, x_host, chunks=None):
         """Host-buffer solve of this shard (the reference's numpy-in / numpy-out
         contract, per rank): K columns in ``chunks`` column chunks through an
         H2D stream -> the solve (current stream, with its two all-gathers) -> a
@@ -250,6 +250,8 @@ class ShardedPlan:
         x_host: pinned CPU tensors (row_hi - row_lo, m, K); returns x_host."""
         torch = self.be.torch
         rows, m, k = (int(v) for v in f_host.shape)
+        if chunks is None:  # as btd_plan_solve_host: >= 256-byte rows (64 columns from K = 256), <= 8
+            chunks = max(1, min(8, k // (64 if k >= 256 else 32)))
         nch = max(1, min(int(chunks), k))
         while k % nch or ((k // nch) % 2 and nch > 1):
             nch -= 1
