@@ -229,9 +229,11 @@ class HelmholtzDD:
         torch = self.torch
         per = self.nsub // self.groups
         K = f.shape[2]
-        out = torch.zeros((per * self.nx, self.Mi, K), dtype=torch.float64, device=f.device)
+        out = torch.empty((per * self.nx, self.Mi, K), dtype=torch.float64, device=f.device)
         for j, (a, e) in enumerate(self.sub[gidx * per:(gidx + 1) * per]):
             out[j * self.nx:(j + 1) * self.nx, : e - a] = f[a:e].permute(1, 0, 2)
+            if e - a < self.Mi:  # identity-padded rows of shorter subdomains (no full zero fill)
+                out[j * self.nx:(j + 1) * self.nx, e - a:] = 0.0
         return out
 
     def solve(self, f):
