@@ -494,13 +494,13 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_bwd_kernel(ChainArg
         cp_async_commit();
     }
   }
-  FragCursor<MP, PF, GPS, 2> cur;
-  cur.seg0 = a.G + (slot0 + nint - 1) * blk + r0 * MP;
-  cur.seg1 = a.S + (slot0 + nint - 1) * blk + r0 * MP;
-  cur.seg2 = nullptr;
-  cur.j = 0; cur.seg = 0; cur.grp = 0; cur.nrows = nint;
+  // factor-fragment stream, rows descending: G_j then S_j per row.  One row pointer into the G
+  // blocks plus the constant G -> S distance (fewer live registers than a per-segment cursor).
+  const double* frow = a.G + (slot0 + nint - 1) * blk + r0 * MP;
+  const int64_t s_off = a.S - a.G;
+  int fseg = 0, fgrp = 0, frows = nint;
   double2 buf[PF][TM];
-  group_load<MP, TM, PF>(buf, cur.ptr(), g, t);
+  group_load<MP, TM, PF>(buf, frow, g, t);
   double y[TM][TN][2];
   if constexpr (NY == 0) load_tile(y, a.X + (lo + nint) * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
   cp_async_wait<(NY > 1 ? NY - 2 : 0)>();
@@ -539,9 +539,15 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_bwd_kernel(ChainArg
     for (int seg = 0; seg < 2; ++seg) {
 #pragma unroll 1
       for (int grp = 0; grp < GPS; ++grp) {
-        cur.advance();
-        const double* nx = cur.ptr();
-        if (nx) nx -= 2 * (int64_t)cur.j * blk;  // cursor rows advance upward; slots go down
+        if (++fgrp == GPS) {  // advance the stream: next group, segment (G -> S), row (down)
+          fgrp = 0;
+          if (++fseg == 2) {
+            fseg = 0;
+            frow -= blk;
+            --frows;
+          }
+        }
+        const double* nx = frows > 0 ? frow + (fseg ? s_off : 0) + fgrp * 8 * PF : nullptr;
         group_mma<MP, TM, TN, PF>(acc, buf, nx, (seg == 0 ? Xq : Xn) + cw0, LD, grp * PF, g, t);
       }
     }
