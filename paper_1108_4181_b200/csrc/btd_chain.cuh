@@ -300,28 +300,6 @@ BTD_DEVINL void group_load(double2 (&buf)[PF][TM], const double* __restrict__ p,
     for (int i = 0; i < TM; ++i) buf[u][i] = ldg_cg2(p + (i * 8 + g) * MP + 8 * u + 2 * t);
 }
 
-// Walks the factor-fragment stream (row j, segment, group) in execution order.
-template <int MP, int PF, int GPS, int NSEG>
-struct FragCursor {
-  const double* seg0;
-  const double* seg1;
-  const double* seg2;
-  int j, seg, grp, nrows;
-  BTD_DEVINL const double* ptr() const {
-    if (j >= nrows) return nullptr;
-    const double* b = seg == 0 ? seg0 : (seg == 1 ? seg1 : seg2);
-    return b + (int64_t)j * MP * MP + grp * 8 * PF;
-  }
-  BTD_DEVINL void advance() {
-    if (++grp == GPS) {
-      grp = 0;
-      if (++seg == NSEG) {
-        seg = 0;
-        ++j;
-      }
-    }
-  }
-};
 
 // Forward sweep.  Per interior row j, three segments stream through the same
 // register ring:  seg0 acc += AD_j y_{j-1};  seg1 ser += Tb_{j-1} y_{j-1};
@@ -369,13 +347,14 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_fwd_kernel(ChainArg
       cp_async_commit();
   }
 
-  FragCursor<MP, PF, GPS, 3> cur;
-  cur.seg0 = a.AD + slot0 * blk + r0 * MP;
-  cur.seg1 = a.Tb + slot0 * blk + r0 * MP;  // row j uses Tb_{j-1} (offset below; row 0 reuses Tb_0 x 0)
-  cur.seg2 = a.Dinv + slot0 * blk + r0 * MP;
-  cur.j = 0; cur.seg = 0; cur.grp = 0; cur.nrows = nint;
+  // factor-fragment stream, rows ascending: AD_j, Tb_{j-1} (row 0 reuses Tb_0 against y_{-1} = 0),
+  // Dinv_j.  One row pointer into the AD blocks plus constant offsets to the Tb / Dinv pools.
+  const double* frow = a.AD + slot0 * blk + r0 * MP;
+  const int64_t tb_off = a.Tb - a.AD, dinv_off = a.Dinv - a.AD;
+  int fseg = 0, fgrp = 0, frows = nint;
+  bool frow0 = true;  // the stream is still in row 0 (its Tb segment uses Tb_0, not Tb_{-1})
   double2 buf[PF][TM];
-  group_load<MP, TM, PF>(buf, cur.ptr(), g, t);
+  group_load<MP, TM, PF>(buf, frow, g, t);
   cp_async_wait<NF - 2>();
   __syncthreads();
 
@@ -408,9 +387,18 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_fwd_kernel(ChainArg
     for (int seg = 0; seg < 3; ++seg) {
 #pragma unroll 1
       for (int grp = 0; grp < GPS; ++grp) {
-        cur.advance();
-        const double* nx = cur.ptr();
-        if (nx && cur.seg == 1 && cur.j > 0) nx -= blk;  // Tb_{j-1}
+        if (++fgrp == GPS) {  // advance the stream: next group, segment, row
+          fgrp = 0;
+          if (++fseg == 3) {
+            fseg = 0;
+            frow += blk;
+            --frows;
+            frow0 = false;
+          }
+        }
+        const double* nx = nullptr;
+        if (frows > 0)
+          nx = frow + (fseg == 0 ? 0 : (fseg == 1 ? tb_off - (frow0 ? 0 : blk) : dinv_off)) + fgrp * 8 * PF;
         if (seg == 0)
           group_mma<MP, TM, TN, PF>(acc, buf, nx, Ys + cw0, LD, grp * PF, g, t);
         else if (seg == 1)
