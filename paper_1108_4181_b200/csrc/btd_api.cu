@@ -683,20 +683,30 @@ void launch_inv(btd_plan& pl, int nbatch, const double* in, const int64_t* idx_i
 }
 
 // ---------------------------------------------------------------- chain kernels
-template <int MP, int KT, int WR, int WC, int NF = -1, int NY = -1, int PF = -1, int MINB = 1>
+template <int MP, int KT, int WR, int WC, int NF = -1, int NY = -1, int PF = -1, int MINB = 1, int FULL = 0>
 void launch_chain_t(const ChainArgs& a, bool fwd, cudaStream_t st) {
   using Cfg = ChainCfg<MP, KT, WR, WC, NF, NY, PF>;
   const size_t smem = (size_t)(fwd ? Cfg::FWD_BUFS : Cfg::BWD_BUFS) * MP * Cfg::LD * sizeof(double);
   const int64_t ntile = (a.K + KT - 1) / KT;
   dim3 grid((unsigned)ntile, (unsigned)a.nr);
   if (fwd) {
-    set_smem_attr((const void*)chain_fwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB>, smem);
-    chain_fwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB><<<grid, Cfg::NT, smem, st>>>(a);
+    set_smem_attr((const void*)chain_fwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB, FULL>, smem);
+    chain_fwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB, FULL><<<grid, Cfg::NT, smem, st>>>(a);
   } else {
-    set_smem_attr((const void*)chain_bwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB>, smem);
-    chain_bwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB><<<grid, Cfg::NT, smem, st>>>(a);
+    set_smem_attr((const void*)chain_bwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB, FULL>, smem);
+    chain_bwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB, FULL><<<grid, Cfg::NT, smem, st>>>(a);
   }
   CK_LAUNCH();
+}
+
+// Default shapes: a bounds-check-free variant when every tile is full (block order == MP,
+// K a multiple of the column tile, K even).
+template <int MP, int KT, int WR, int WC, int NF = -1, int NY = -1, int PF = -1>
+void launch_chain_auto(const ChainArgs& a, bool fwd, cudaStream_t st) {
+  if (a.m == MP && a.K % KT == 0 && a.K % 2 == 0)
+    launch_chain_t<MP, KT, WR, WC, NF, NY, PF, 1, 1>(a, fwd, st);
+  else
+    launch_chain_t<MP, KT, WR, WC, NF, NY, PF, 1, 0>(a, fwd, st);
 }
 
 template <int MP, int NW, int NSTG>
@@ -792,8 +802,8 @@ void launch_chain_slice(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t s
       // measured best (c2, profiles/r01_chain_ab.txt): 128-column tiles of 2 x 8 warps with
       // per-column-group barriers in both directions (bwd 9.96 -> 9.54 ms vs 32-column tiles);
       // forward factor fragments 8 pair steps ahead (13.76 -> 13.66 ms)
-      else if (fwd) launch_chain_t<64, 128, 8, 2, 2, 0, 8>(a, fwd, st);
-      else launch_chain_t<64, 128, 8, 2, 2, 0>(a, fwd, st);
+      else if (fwd) launch_chain_auto<64, 128, 8, 2, 2, 0, 8>(a, fwd, st);
+      else launch_chain_t<64, 128, 8, 2, 2, 0>(a, fwd, st);  // (the bounds-check-free variant is 7% slower here)
       break;
     case 128:
       if (variant == 1) launch_chain_t<128, 64, 16, 2>(a, fwd, st);
@@ -804,7 +814,7 @@ void launch_chain_slice(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t s
       else if (variant == 6) launch_chain_t<128, 32, 16, 1>(a, fwd, st);
       else if (variant == 7) launch_chain_t<128, 64, 16, 1, -1, -1, 8>(a, fwd, st);
       else if (variant == 8) launch_chain_t<128, 64, 16, 1, -1, -1, 16>(a, fwd, st);
-      else launch_chain_t<128, 64, 16, 1>(a, fwd, st);  // measured best on the c3dd interiors (+7%)
+      else launch_chain_auto<128, 64, 16, 1>(a, fwd, st);  // measured best on the c3dd interiors (+7%)
       break;
     case 256:
       if (variant == 1) launch_chain_t<256, 32, 16, 1>(a, fwd, st);
@@ -826,8 +836,8 @@ void launch_chain_slice(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t s
       else if (variant == 17) launch_chain_t<256, 16, 16, 1, 2, 3, 4>(a, fwd, st);
       // measured (c1, profiles/r01_chain_ab.txt): forward factor fragments 8 pair steps ahead
       // (13.08 -> 12.74 ms; 2 ahead: 17.1 ms), 32-warp CTAs backward (-4%)
-      else if (fwd) launch_chain_t<256, 16, 16, 1, -1, -1, 8>(a, fwd, st);
-      else launch_chain_t<256, 32, 32, 1>(a, fwd, st);
+      else if (fwd) launch_chain_auto<256, 16, 16, 1, -1, -1, 8>(a, fwd, st);
+      else launch_chain_auto<256, 32, 32, 1>(a, fwd, st);
       break;
     default: fail(BTD_ERR_UNSUPPORTED, "no chain kernel for this block order");
   }

@@ -129,9 +129,22 @@ BTD_DEVINL void zero_acc(double (&acc)[TM][TN][2]) {
 }
 
 // C-layout tile <-> global (rows r < rmax, cols c < K), row stride K.
-template <int TM, int TN>
+// FULL: every row < rmax and column pair < K (block order == MP, K a multiple of the tile
+// width, K even) -- no bounds checks, 16-byte accesses only.
+template <int TM, int TN, bool FULL = false>
 BTD_DEVINL void load_tile(double (&acc)[TM][TN][2], const double* __restrict__ P, int64_t K,
                           int r0, int64_t c0, int rmax, int g, int t, bool vec) {
+  if constexpr (FULL) {
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(P + (int64_t)(r0 + i * 8 + g) * K + c0 + j * 8 + 2 * t));
+        acc[i][j][0] = v.x;
+        acc[i][j][1] = v.y;
+      }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -154,9 +167,18 @@ BTD_DEVINL void load_tile(double (&acc)[TM][TN][2], const double* __restrict__ P
     }
 }
 
-template <int TM, int TN>
+template <int TM, int TN, bool FULL = false>
 BTD_DEVINL void store_tile(const double (&acc)[TM][TN][2], double* __restrict__ P, int64_t K,
                            int r0, int64_t c0, int rmax, int g, int t, bool vec) {
+  if constexpr (FULL) {
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+        __stcg(reinterpret_cast<double2*>(P + (int64_t)(r0 + i * 8 + g) * K + c0 + j * 8 + 2 * t),
+               make_double2(acc[i][j][0], acc[i][j][1]));
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -304,7 +326,7 @@ BTD_DEVINL void group_load(double2 (&buf)[PF][TM], const double* __restrict__ p,
 // Forward sweep.  Per interior row j, three segments stream through the same
 // register ring:  seg0 acc += AD_j y_{j-1};  seg1 ser += Tb_{j-1} y_{j-1};
 // seg2 acc += Dinv_j f_g.  (At j = 0, y_{-1} = 0 and seg1 reuses Tb_0.)
-template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1, int MINB_ = 1>
+template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1, int MINB_ = 1, int FULL_ = 0>
 __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_fwd_kernel(ChainArgs a) {
   using Cfg = ChainCfg<MP, KT, WR, WC, NF_, NY_, PF_>;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, LD = Cfg::LD, NT = Cfg::NT, PF = Cfg::PF, GPS = Cfg::GPS;
@@ -409,7 +431,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_fwd_kernel(ChainArg
     }
     group_sync<WR, WC>(wc);
     store_smem(acc, Ys, LD, r0, cw0, g, t);
-    store_tile(acc, a.X + gr * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
+    store_tile<TM, TN, FULL_ != 0>(acc, a.X + gr * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
     zero_acc(acc);
     cp_async_wait<NF - 2>();  // row j+1's F tile has landed
     group_sync<WR, WC>(wc);
@@ -434,7 +456,7 @@ BTD_DEVINL void load_smem(double (&acc)[TM][TN][2], const double* Ys, int ld, in
 
 // Backward sweep: per row j (descending) two segments through one ring:
 // seg0 acc += G_j x~_q ; seg1 acc += S_j x_{j+1}, with acc initialised to y_j.
-template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1, int MINB_ = 1>
+template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1, int MINB_ = 1, int FULL_ = 0>
 __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_bwd_kernel(ChainArgs a) {
   using Cfg = ChainCfg<MP, KT, WR, WC, NF_, NY_, PF_>;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, LD = Cfg::LD, NT = Cfg::NT, PF = Cfg::PF, GPS = Cfg::GPS;
@@ -521,7 +543,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_bwd_kernel(ChainArg
       for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int c = 0; c < TN; ++c) { acc[i][c][0] = y[i][c][0]; acc[i][c][1] = y[i][c][1]; }
-      if (j > 0) load_tile(y, a.X + (gr - 1) * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
+      if (j > 0) load_tile<TM, TN, FULL_ != 0>(y, a.X + (gr - 1) * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
     }
 #pragma unroll 1
     for (int seg = 0; seg < 2; ++seg) {
@@ -541,7 +563,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_bwd_kernel(ChainArg
     }
     group_sync<WR, WC>(wc);
     store_smem(acc, Xn, LD, r0, cw0, g, t);
-    store_tile(acc, a.X + gr * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
+    store_tile<TM, TN, FULL_ != 0>(acc, a.X + gr * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
     if constexpr (NY > 1) cp_async_wait<NY - 2>();
     group_sync<WR, WC>(wc);
   }

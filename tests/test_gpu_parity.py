@@ -246,3 +246,16 @@ def test_more_device_ranges_than_grid_y(m, k):
     ref = coracle.CPlan(d, lo, up, ranks).solve(f)
     assert O.max_rel_err(x, ref) <= 1e-9
     assert O.rel_residual(d, lo, up, x, f) <= 1e-10
+
+
+@pytest.mark.parametrize("n,m,k,ranks", [(40, 64, 128, 4), (24, 256, 32, 3), (30, 128, 64, 3), (33, 64, 256, 5)])
+def test_full_tile_chain_variants(n, m, k, ranks):
+    """Block order == the kernel's MP and K a multiple of its column tile: the default chain
+    shapes take their bounds-check-free variants; parity against the oracle."""
+    d, lo, up, f = configs.dominant_numpy(n, m, k, seed=n + k)
+    plan = plan_build(BlockTriMatrix(d, lo, up), ranks)
+    import torch
+
+    x = plan_solve(plan, torch.from_numpy(f).cuda()).cpu().numpy()
+    ref = O.plan_solve(O.plan_build(d, lo, up, ranks), f)
+    _check(d, lo, up, x, f, ref)
