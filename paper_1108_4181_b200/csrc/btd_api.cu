@@ -1715,6 +1715,8 @@ const SplitK* step_split(btd_plan& pl, int cnt, int64_t K) {
 }
 
 // dst[dst_idx[b]] = src[src_idx[b]], blocks of `per` doubles
+}  // namespace
+namespace btd {  // (::btd: launch lists attribute it to this library)
 __global__ void copy_blocks_kernel(double* dst, const int64_t* dst_idx, const double* src, const int64_t* src_idx,
                                    int count, int64_t per) {
   for (int b = blockIdx.y; b < count; b += gridDim.y) {
@@ -1724,6 +1726,8 @@ __global__ void copy_blocks_kernel(double* dst, const int64_t* dst_idx, const do
       d[e] = sp[e];
   }
 }
+}  // namespace btd
+namespace {
 
 // Algorithm 1, level part: x~_k = z_node + E x~_{lo-1} + H x~_{hi+1}, level by level.
 void solve_levels(btd_plan& pl, int64_t K, cudaStream_t st) {
@@ -1734,7 +1738,7 @@ void solve_levels(btd_plan& pl, int64_t K, cudaStream_t st) {
     if (lev.count <= 0) continue;
     if (lev.copy_only) {  // the root level: x~_k = z_root, a copy, not a GEMM + split-K reduction
       dim3 grid((unsigned)std::min<int64_t>((mpK + 255) / 256, 592), (unsigned)std::min(lev.count, 65535));
-      copy_blocks_kernel<<<grid, 256, 0, st>>>(xt, lev.c_idx, z, lev.z_idx, lev.count, mpK);
+      btd::copy_blocks_kernel<<<grid, 256, 0, st>>>(xt, lev.c_idx, z, lev.z_idx, lev.count, mpK);
       CK_LAUNCH();
       continue;
     }
@@ -1933,12 +1937,18 @@ void solve_shard_a(btd_plan& pl, const double* F, double* X, int64_t K, double* 
               {term(mk(pl.pool.d(), pl.cout_fc, 0, blk, mp), mk(X, pl.cout_row, 0, mK, K), m)}, st);
 }
 
+}  // namespace
+namespace btd {  // (::btd: launch lists attribute it to this library)
 __global__ void add_block_kernel(double* dst, const double* src, int64_t n) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     dst[e] += src[e];
 }
+}  // namespace btd
+namespace {
 
 // z_b = sum over ranks (fixed order) of the partial series sums of crossing node c
+}  // namespace
+namespace btd {  // (::btd: launch lists attribute it to this library)
 __global__ void sum_ranks_kernel(const double* part_all, int world, int ncross, int64_t per, const int64_t* node,
                                  double* z) {
   for (int c = blockIdx.y; c < ncross; c += gridDim.y) {
@@ -1950,6 +1960,8 @@ __global__ void sum_ranks_kernel(const double* part_all, int world, int ncross, 
     }
   }
 }
+}  // namespace btd
+namespace {
 
 // Sharded phase B: finish f~ of the first owned range with the previous rank's carry,
 // local series sums of nodes inside this rank, partial sums of crossing nodes.
@@ -1957,7 +1969,7 @@ void solve_shard_b(btd_plan& pl, const double* carry_all, double* partial_out, i
   const int64_t mp = pl.mp, mpK = mp * K;
   double* ft = pl.S().ft.d();
   if (pl.rank >= 1) {
-    add_block_kernel<<<64, 256, 0, st>>>(ft + pl.q0 * mpK, carry_all + (int64_t)(pl.rank - 1) * mpK, mpK);
+    btd::add_block_kernel<<<64, 256, 0, st>>>(ft + pl.q0 * mpK, carry_all + (int64_t)(pl.rank - 1) * mpK, mpK);
     CK_LAUNCH();
   }
   if (pl.fused_shard) {
@@ -1985,7 +1997,7 @@ void solve_shard_c(btd_plan& pl, const double* partial_all, const double* F, dou
   }
   if (pl.ncross) {
     dim3 grid((unsigned)std::min<int64_t>((mpK + 255) / 256, 64), (unsigned)std::min(pl.ncross, 65535));
-    sum_ranks_kernel<<<grid, 256, 0, st>>>(partial_all, pl.world, pl.ncross, mpK, pl.cross_node, pl.S().zbuf.d());
+    btd::sum_ranks_kernel<<<grid, 256, 0, st>>>(partial_all, pl.world, pl.ncross, mpK, pl.cross_node, pl.S().zbuf.d());
     CK_LAUNCH();
   }
   solve_levels(pl, K, st);

@@ -24,7 +24,7 @@ for c in ${NCU_CONFIGS:-c1 c2 c4 c3}; do
   echo "ncu $c rc=$?"
   python tools/ncu_summary.py $T/prof_$c.ncu-rep > $OUT/ncu_full_$c.txt 2>&1
   python tools/launch_shares.py $OUT/launch_shares_$c.json $c:$T/launches_$c.csv:$T/plain_$c.log > /dev/null 2>&1
-  grep -E "btd::|Kernel Name" $T/launches_$c.csv | tail -n 400 > $OUT/launches_$c.csv
+  grep -E "btd::|anonymous namespace|Kernel Name" $T/launches_$c.csv | tail -n 400 > $OUT/launches_$c.csv
   cp $T/plain_$c.log $OUT/
 done
 du -sh $OUT

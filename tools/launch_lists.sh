@@ -11,7 +11,7 @@ for c in ${CONFIGS:-c1 c2 c3 c4 c0}; do
   python - "$T/launches_$c.csv" "$OUT/launches_$c.csv" <<'PY'
 import sys
 lines = open(sys.argv[1]).read().splitlines()
-keep = [l for l in lines if "btd::" in l or "Kernel Name" in l]
+keep = [l for l in lines if "btd::" in l or "anonymous namespace" in l or "Kernel Name" in l]
 open(sys.argv[2], "w").write("\n".join(keep[-400:]) + "\n")
 PY
 done

@@ -17,7 +17,8 @@ for arg in sys.argv[2:]:
     t = []
     for r in rows[hdr + 1:]:
         # only this library's kernels (the bench also runs cuBLAS / torch kernels)
-        if len(r) > vi and r[mi] == "gpu__time_duration.sum" and "btd::" in r[ki]:
+        # (helper kernels in btd_api.cu's anonymous namespace count too: gpu_launches counts them)
+        if len(r) > vi and r[mi] == "gpu__time_duration.sum" and ("btd::" in r[ki] or "anonymous namespace" in r[ki]):
             v = float(r[vi].replace(",", ""))
             u = r[ui]
             v = v / 1000.0 if u in ("ns", "nsecond") else (v * 1000.0 if u in ("ms", "msecond") else v)
