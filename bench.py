@@ -1,28 +1,36 @@
 #!/usr/bin/env python
 """Benchmark of the many-RHS block-tridiagonal dichotomy solve (plan_solve).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl b200|reference]
 
 Metric (BASELINE.json): right-hand-side columns solved per second at a fixed
 matrix.  One *step* = one ``plan_solve`` of the config's K columns, F -> X,
 with the plan (Algorithm 2 step 1) built once beforehand and timed separately.
-Default workload: configs[1] (c1, the 2-D Laguerre acoustic strip operator,
-N=4096 x M=256 blocks, K=256), the configuration the metric is quoted on that
-fits one GPU.
+Default workload: configs[4] (c4, N=2^20 block rows of M=16, K=64), the
+largest configuration -- the one north_star's 1/2/4/8-GPU efficiency target
+is set on (BASELINE.json names no single config for the metric); every other
+config runs with ``--config``.  Inputs are the seeded numpy stream of
+``configs.generate`` -- the same arrays the unmodified reference was run on for
+the full-size goldens (tests/golden/fullsize_*.npz).
 
 * ``value``: device-resident F/X, CUDA events on the solve stream around
-  exactly K steps, max over ranks.  Inputs (F 2.1 GB, factors 10.7 GB for c1)
+  exactly K steps, max over ranks.  Inputs (c4: F 8.6 GB, factors 10.8 GB)
   are larger than the 126 MB L2, so no flush is needed between steps.
-* ``e2e``: the same metric through the reference-facing host API
-  (``btd_plan_solve_host``: pinned host F -> device -> solve -> host X).
-* ``roofline``: the dominant kernel (the fused forward sweep) -- algorithmic
-  flops (or bytes) per launch / its CUDA-event duration, against the fp64
-  tensor peak (cuBLAS DGEMM measured in this run; MEASURED_PEAKS.json has no
-  fp64 entry) or the measured HBM copy bandwidth.
-* ``cpu_baseline``: the CPU oracle (a port of the reference algorithm) on a
-  bounded sample of the same workload, scaled to full-size RHS/s.
-* ``--impl reference``: the reference algorithm on the host cores (the oracle
-  port; /root/reference cannot travel to the GPU box), same metric/config.
+* ``e2e``: the same metric through the public numpy API a reference user
+  calls, ``paper_1108_4181_b200.plan_solve(plan, F_numpy) -> X_numpy``
+  (host F -> device -> solve -> host X every step), wall clock.
+* ``roofline``: the dominant kernel -- algorithmic bytes (or flops) per launch
+  / its CUDA-event duration, against the measured HBM copy bandwidth
+  (MEASURED_PEAKS.json) or the fp64 tensor peak (cuBLAS DGEMM measured in
+  this run; MEASURED_PEAKS.json has no fp64 entry).
+* ``parity``: after the timed region, the solution's golden columns against
+  the reference-written full-size golden and against the C oracle run on the
+  same host arrays (``max_rel_err_vs_oracle``).
+* ``cpu_baseline``: the unmodified reference package (oracle/_ref, built by
+  oracle/build_ref.sh) timed on a bounded sample on the host cores;
+  ``cpu_baseline_port``: the C port of the same algorithm (oracle/).
+* ``--impl reference``: the reference's own plan_solve on the host cores
+  (all of them: one process per core over column slices), same metric/config.
 """
 
 from __future__ import annotations
@@ -267,10 +275,13 @@ def fp64_peak_tflops(torch):
     return 2 * n ** 3 / best / 1e9
 
 
-def make_inputs(name, torch, seed=0):
+def make_inputs(name, seed=0):
+    """Host numpy arrays of config ``name``: the seeded numpy stream of
+    configs.generate -- identical to the arrays the reference was run on for
+    tests/golden/fullsize_<name>.npz."""
     from paper_1108_4181_b200 import configs
 
-    return configs.generate(name, device="cuda", seed=seed)
+    return configs.generate(name, seed=seed)
 
 
 def interior_rows(n, nranges, L):
@@ -281,14 +292,20 @@ def interior_rows(n, nranges, L):
     return tot
 
 
-# --------------------------------------------------------------------------- CPU arm
+# --------------------------------------------------------------------------- CPU arms
+def _oracle_path():
+    p = os.path.join(ROOT, "oracle")
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+
 class CpuSample:
-    """The reference algorithm on the host (oracle/liboracle.so: C port of the
-    reference's compiled path, ranges and column chunks on all host threads)
-    over a bounded sample of config `name`; plan built once (untimed)."""
+    """The C port of the reference algorithm (oracle/liboracle.so; ranges and
+    column chunks on all host threads) over a bounded sample of config `name`;
+    plan built once (untimed).  Reported as ``cpu_baseline_port``."""
 
     def __init__(self, name):
-        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        _oracle_path()
         import coracle
         from paper_1108_4181_b200 import configs
 
@@ -326,16 +343,35 @@ class CpuSample:
         return self.ks / t * self.ns / self.cfg["n"] * self.scale, t
 
 
-def cpu_sample_run(name, steps=1):
+def cpu_port_run(name, steps=1):
     cs = CpuSample(name)
     vals = [cs.step() for _ in range(max(1, steps))]
     v = statistics.median(x[0] for x in vals)
-    t = statistics.median(x[1] for x in vals)
-    return v, t, cs.sample, cs.cores, "port"
+    return {"value": v, "unit": "RHS/s", "cores": cs.cores, "kind": "port", "sample": cs.sample}
+
+
+def cpu_reference_run(name, steps=2, warmup=1, workers=None):
+    """The unmodified reference's plan_solve (oracle/refcpu.py) on the host cores."""
+    _oracle_path()
+    import refcpu
+
+    if not refcpu.available():
+        return None
+    rs = refcpu.RefSample(name, workers=workers)
+    try:
+        for _ in range(warmup):
+            rs.step()
+        res = [rs.step() for _ in range(max(1, steps))]
+    finally:
+        rs.close()
+    ts = [r[1] for r in res]
+    value = rs.cfg["k"] * len(ts) / sum(ts) * rs.scale
+    return {"value": value, "unit": "RHS/s", "cores": rs.workers, "kind": "reference", "sample": rs.sample,
+            "ms_per_step": 1e3 * sum(ts) / len(ts)}
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU algorithm on this host's cores
+    """--impl reference: the reference's own plan_solve on this host's cores
     (rank 0 only; other ranks exit without work)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -344,25 +380,71 @@ def run_reference(args):
     from paper_1108_4181_b200 import configs
 
     cfg = configs.CONFIGS[name]
-    cs = CpuSample(name)
-    for _ in range(args.warmup):
-        cs.step()
-    res = [cs.step() for _ in range(args.steps)]
-    ts = [r[1] for r in res]
-    value = cs.ks * args.steps / sum(ts) * cs.ns / cfg["n"] * cs.scale
+    _oracle_path()
+    import refcpu
+
+    if refcpu.available():
+        cb = cpu_reference_run(name, steps=args.steps, warmup=args.warmup)
+    else:  # the reference could not be built: the C port of its algorithm
+        cs = CpuSample(name)
+        for _ in range(args.warmup):
+            cs.step()
+        res = [cs.step() for _ in range(args.steps)]
+        ts = [r[1] for r in res]
+        cb = {"value": cs.ks * len(ts) / sum(ts) * cs.ns / cfg["n"] * cs.scale, "unit": "RHS/s",
+              "cores": cs.cores, "kind": "port", "sample": cs.sample, "ms_per_step": 1e3 * sum(ts) / len(ts)}
+    value = cb["value"]
     line = {
         "impl": "reference", "metric": "rhs_columns_per_second", "value": value, "unit": "RHS/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * sum(ts) / len(ts), "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": cb.pop("ms_per_step"), "higher_is_better": True,
+        "scaling": "strong" if name in ("c0", "c1", "c2") else "weak-subdomains",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy, BASELINE.json distributions)",
-        "config": {"workload": name, "n": cfg["n"], "m": cfg["m"], "k": cfg["k"], "sample_ranks": cs.ps},
-        "cpu_baseline": {"value": value, "unit": "RHS/s", "cores": cs.cores, "kind": "port", "sample": cs.sample},
+        "config": {"workload": name, "n": cfg["n"], "m": cfg["m"], "k": cfg["k"]},
+        "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "RHS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
 
 
 # --------------------------------------------------------------------------- GPU arm
+def parity_report(name, X, host, rows, ranks):
+    """Golden columns of the GPU solution X (device, rows [lo, hi) of the global
+    solution) against the reference-written full-size golden and the C oracle
+    run live on the same host arrays."""
+    _oracle_path()
+    import parity
+
+    from paper_1108_4181_b200 import configs
+
+    g, meta = parity.golden(name)
+    if g is None or rows != (0, configs.CONFIGS[name]["n"]):
+        return None
+    cols = meta["cols"]
+    x_cols = X[:, :, cols].cpu().numpy()
+    out = {"cols": cols}
+    rep = parity.compare_golden(name, x_cols)
+    out["vs_reference_golden"] = rep
+    diag, lower, upper, F = host
+    f_cols = np.ascontiguousarray(F[:, :, cols])
+    out["inputs_match_golden"] = (parity.sha_inputs(diag, lower, upper, f_cols) == meta["sha_inputs"]
+                                  if configs.CONFIGS[name]["kind"] != "schur" else "S formed by BLAS (rounding)")
+    if configs.CONFIGS[name]["kind"] == "schur":
+        out["vs_oracle"] = None  # M = 2048 CPU plan takes minutes; the golden holds every row
+        out["max_rel_err_vs_oracle"] = rep["max_rel_err_sampled_rows"]
+        out["oracle"] = "reference golden (all 63 rows)"
+        return out
+    import coracle
+
+    t0 = time.perf_counter()
+    p_or = max(ranks, min(coracle.threads(), configs.CONFIGS[name]["n"] // 8))
+    ref = parity.oracle_columns(diag, lower, upper, f_cols, p_or)
+    out["max_rel_err_vs_oracle"] = parity.max_rel_err(x_cols, ref)
+    out["oracle"] = (f"C oracle (oracle/liboracle.so), all {x_cols.shape[0]} block rows, P={p_or}, "
+                     f"{time.perf_counter() - t0:.1f} s")
+    return out
+
+
 def run_b200(args):
     import ctypes
 
@@ -386,6 +468,7 @@ def run_b200(args):
         os.environ.setdefault("MASTER_PORT", "29517")
         dist.init_process_group(backend, rank=rank, world_size=world,
                                 device_id=torch.device("cuda", local) if backend == "nccl" else None)
+    import paper_1108_4181_b200 as btd
     from paper_1108_4181_b200 import _native, configs, plan_build_arrays
     from paper_1108_4181_b200.distributed import ShardedPlan
 
@@ -395,10 +478,12 @@ def run_b200(args):
     n, m, K = cfg["n"], cfg["m"], cfg["k"]
     lib = _native.load()
     stream = torch.cuda.current_stream()
-    sp = ctypes.c_void_p(stream.cuda_stream)
 
-    # every rank draws the same global matrix / RHS (seeded, on device) and keeps its rows
-    diag, lower, upper, F = make_inputs(name, torch)
+    # every rank draws the same global matrix / RHS (seeded numpy stream) and keeps its rows
+    t0 = time.perf_counter()
+    host = make_inputs(name)
+    gen_s = time.perf_counter() - t0
+    diag, lower, upper = (torch.from_numpy(a).cuda() for a in host[:3])
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     if not sharded:
@@ -409,17 +494,18 @@ def run_b200(args):
     else:
         plan = ShardedPlan(diag, lower, upper, ranks, split=split)
         row_lo, row_hi = plan.row_lo, plan.row_hi
-        F = F[row_lo:row_hi].contiguous()
         info = plan.be.info(plan.h)
         nranges, L, mode, fbytes = plan.nranges, plan.L, int(info.mode), int(info.factor_bytes)
         handle = plan.h
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
-    del diag, lower, upper
-    torch.cuda.empty_cache()
+    Fh = np.ascontiguousarray(host[3][row_lo:row_hi])
+    F = torch.from_numpy(Fh).cuda()
     X = torch.empty_like(F)
 
     if not sharded:
+        sp = ctypes.c_void_p(stream.cuda_stream)
+
         def solve():
             st = lib.btd_plan_solve(handle, ctypes.c_void_p(F.data_ptr()), ctypes.c_void_p(X.data_ptr()), K, sp)
             if st:
@@ -447,6 +533,7 @@ def run_b200(args):
         if dist:
             dist.barrier()
     ms = e0.elapsed_time(e1)
+    ms_rank = ms
     if dist:
         tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -465,45 +552,64 @@ def run_b200(args):
     lib.btd_plan_phase_times(handle, buf, ctypes.byref(nsv), 1)
     lib.btd_plan_set_profiling(handle, 0)
     ph = [buf[i] / max(1, nsv.value) for i in range(4)]
+    per_rank = None
+    if dist:
+        vals = torch.tensor([ms_rank / args.steps] + ph, device="cuda", dtype=torch.float64)
+        allv = torch.empty(world * vals.numel(), device="cuda", dtype=torch.float64)
+        dist.all_gather_into_tensor(allv, vals)
+        allv = allv.view(world, -1).cpu().tolist()
+        per_rank = [{"rank": r, "ms_per_step": v[0], "forward": v[1], "interface_tree": v[2], "backward": v[3],
+                     "total": v[4]} for r, v in enumerate(allv)]
 
     res = None
     if not args.no_check:
-        res = (residual_check_sharded(torch, dist, name, X, F, configs, row_lo, row_hi) if sharded
-               else residual_check(torch, name, X, F, configs))
+        res = (residual_check_sharded(torch, dist, X, F, diag, lower, upper, row_lo, row_hi) if sharded
+               else residual_check(torch, X, F, diag, lower, upper))
+    del diag, lower, upper
+    torch.cuda.empty_cache()
+    par = None
+    if not args.no_check and rank == 0:
+        try:
+            par = parity_report(name, X, host, (row_lo, row_hi), ranks)
+        except Exception as exc:  # the report must not kill the bench line
+            par = {"error": f"{type(exc).__name__}: {exc}"}
 
-    # e2e through the host-memory API: pinned host F -> device -> solve -> host X
+    # e2e through the public host-memory API: numpy F -> device -> solve -> numpy X
     e2e = None
     if not args.no_e2e:
-        Fh = F.cpu().pin_memory()
-        Xh = torch.empty_like(Fh).pin_memory()
+        del F, X
+        torch.cuda.empty_cache()
         if not sharded:
             def solve_host():
-                st = lib.btd_plan_solve_host(handle, ctypes.c_void_p(Fh.data_ptr()), ctypes.c_void_p(Xh.data_ptr()),
-                                             K, sp)
-                if st:
-                    _native.check(st)
+                return btd.plan_solve(plan, Fh)
+            api = "paper_1108_4181_b200.plan_solve(plan, numpy (n, m, k)) -> numpy"
         else:
+            Fp = torch.from_numpy(Fh).pin_memory()
+            Xp = torch.empty_like(Fp).pin_memory()
+
             def solve_host():
-                plan.solve_host(Fh, Xh)
-        solve_host()
-        torch.cuda.synchronize()
+                plan.solve_host(Fp, Xp)
+                return Xp
+            api = "ShardedPlan.solve_host(pinned host rows) (per-rank host pipeline)"
+        xh = solve_host()  # warm: pins F once, fills the pinned solution pool
+        del xh
         if dist:
             dist.barrier()
-        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         esteps = max(1, min(args.steps, 5))
-        h0.record(stream)
+        t0 = time.perf_counter()
         for _ in range(esteps):
-            solve_host()
-        h1.record(stream)
-        h1.synchronize()
-        ems = h0.elapsed_time(h1)
+            xh = solve_host()
+            _ = float(xh[-1, -1, -1])  # the step's result is read on the host
+        ems = (time.perf_counter() - t0) * 1e3
         if dist:
             tt = torch.tensor([ems], device="cuda", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = float(tt.item())
-        nbytes = Fh.numel() * 8
+        nbytes = Fh.nbytes
         e2e = {"value": K * esteps / (ems / 1e3), "unit": "RHS/s", "h2d_bytes_per_step": nbytes,
-               "d2h_bytes_per_step": nbytes, "steps": esteps}
+               "d2h_bytes_per_step": nbytes, "steps": esteps, "ms_per_step": ems / esteps, "api": api,
+               "timing": "host wall clock around the blocking API calls, max over ranks"}
+        del xh
 
     if rank != 0:
         if dist:
@@ -528,29 +634,37 @@ def run_b200(args):
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = ncu_traffic(name)
     roof["kernel"] = (("stream_fwd_kernel (TMA bulk-copy ring)" if m <= 32 and K % 2 == 0 else "chain_fwd_kernel")
-                      if mode == 0 else "gemm_pipe_kernel (mode 1: one batched GEMM per row step)")
+                      if mode == 0 else "gemm_tma_kernel (mode 1: one batched TMA GEMM per row step)")
+    roof["algorithmic_per_launch"] = (f"{fwd_bytes:.4e} B = 8(3M^2+2MK) x {nint:.0f} interior rows" if hbm_bound
+                                      else f"{fwd_flops:.4e} flop = 6M^2K x {nint:.0f} interior rows")
     roof["peak_source"] = ("cuBLAS DGEMM 4096^3 measured in this run (fp64 tensor; MEASURED_PEAKS.json has no fp64)"
-                           if not hbm_bound else "MEASURED_PEAKS.json hbm_gbs")
+                           if not hbm_bound else "MEASURED_PEAKS.json hbm_gbs (burst copy)")
     t_roof = max(tot_flops / (fp64 * 1e12), tot_bytes / (hbm * 1e9))
     clocks = clk.summary()
 
-    cpu = None
+    cpu = cpu_port = None
     if world == 1 and not args.no_cpu:
-        v, t, sample, cores, kind = cpu_sample_run(name)
-        cpu = {"value": v, "unit": "RHS/s", "cores": cores, "kind": kind, "sample": sample}
+        try:
+            cpu = cpu_reference_run(name)
+        except Exception as exc:
+            cpu = {"error": f"{type(exc).__name__}: {exc}"}
+        cpu_port = cpu_port_run(name)
+        if cpu is None:
+            cpu = cpu_port
 
     line = {
         "metric": "rhs_columns_per_second", "value": value, "unit": "RHS/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong" if name in ("c0", "c1", "c2") else "weak-subdomains",
         "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded torch Philox on device; BASELINE.json distributions)",
+        "data": "synthetic (seeded numpy stream of configs.generate, BASELINE.json distributions; "
+                "identical to the reference's full-size golden inputs)",
         "config": {"workload": name, "n": n, "m": m, "k": K, "ranks": ranks, "split": split,
                    "device_ranges": nranges, "L": L, "mode": mode,
                    "parallelism": f"rows sharded over {world} GPUs (NCCL all-gather of interface pairs)"
                    if sharded else "single GPU",
                    "l2": "inputs larger than L2 (F %.2f GB, factors %.2f GB per GPU)" % (
-                       F.numel() * 8 / 1e9, fbytes / 1e9)},
+                       Fh.nbytes / 1e9, fbytes / 1e9)},
         "roofline": roof,
         "solve_roofline": {"flops_per_gpu": tot_flops, "bytes_per_gpu": tot_bytes,
                            # SURVEY 8(d) companions: strict lower bound 8(5M^2 + 2MK) and the
@@ -560,10 +674,15 @@ def run_b200(args):
                            "t_roof_ms": t_roof * 1e3,
                            "frac": t_roof * 1e3 / ms_step, "fp64_tflops_peak": fp64, "hbm_gbs_peak": hbm},
         "phases_ms": {"forward": ph[0], "interface_tree": ph[1], "backward": ph[2], "total": ph[3]},
+        "per_rank": per_rank,
         "plan_build_s": build_s,
+        "input_generation_s": gen_s,
         "rel_residual": res,
+        "max_rel_err_vs_oracle": par.get("max_rel_err_vs_oracle") if isinstance(par, dict) else None,
+        "parity": par,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "cpu_baseline_port": cpu_port,
         "clocks": clocks,
         "gpu_launches": launches,
     }
@@ -582,23 +701,21 @@ def ncu_traffic(name):
         return None
 
 
-def residual_check(torch, name, X, F, configs):
-    """max|P X - F| / max|F| on the device (ref cli.py:211-214), matrix regenerated."""
-    diag, lower, upper, _ = configs.generate(name, device="cuda", k=0)
+def residual_check(torch, X, F, diag, lower, upper):
+    """max|P X - F| / max|F| on the device (ref cli.py:211-214)."""
     y = torch.bmm(diag, X)
     y[1:] -= torch.bmm(lower, X[:-1])
     y[:-1] -= torch.bmm(upper, X[1:])
     r = ((y - F).abs().max() / F.abs().max()).item()
-    del diag, lower, upper, y
+    del y
     torch.cuda.empty_cache()
     return r
 
 
-def residual_check_sharded(torch, dist, name, X, F, configs, lo, hi):
+def residual_check_sharded(torch, dist, X, F, diag, lower, upper, lo, hi):
     """Sharded form of residual_check: each rank's rows [lo, hi) with the neighbour
     ranks' boundary rows of X exchanged (one all-gather of first/last rows); the
     max over ranks of max|P X - F| over the max over ranks of max|F|."""
-    diag, lower, upper, _ = configs.generate(name, device="cuda", k=0)
     n = diag.shape[0]
     world, rank = dist.get_world_size(), dist.get_rank()
     edge = torch.stack([X[0], X[-1]]).contiguous()
@@ -618,7 +735,7 @@ def residual_check_sharded(torch, dist, name, X, F, configs, lo, hi):
         y[:-1] -= torch.bmm(upper[lo:hi - 1], X[1:])
     t = torch.tensor([(y - F).abs().max().item(), F.abs().max().item()], dtype=torch.float64, device=X.device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    del diag, lower, upper, y
+    del y
     torch.cuda.empty_cache()
     return float(t[0] / t[1])
 
@@ -677,7 +794,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c1"), choices=sorted(BENCH_CFG) + ["c3dd"])
+    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c4"), choices=sorted(BENCH_CFG) + ["c3dd"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ranks", type=int, default=0)
     ap.add_argument("--split", type=int, default=0)

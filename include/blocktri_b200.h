@@ -182,6 +182,18 @@ int btd_plan_phase_times(btd_plan* plan, double* ms_out, int64_t* nsolves, int r
 int btd_copy_columns(double* host, int64_t rows, int64_t K, int64_t c0, int64_t kc, double* dev, int to_device,
                      void* stream);
 
+/* Host memory for the numpy path (ref dichotomy.py:358-390 takes and returns
+ * host arrays).  The pipelined btd_plan_solve_host overlaps its copies with the
+ * solve only on page-locked memory:
+ *   btd_host_pin    page-locks an existing host range (cudaHostRegister);
+ *                   *was_pinned = 1 (and nothing is done) when it already is;
+ *   btd_host_unpin  undoes btd_host_pin;
+ *   btd_host_alloc / btd_host_free  page-locked allocations (solution arrays). */
+int btd_host_pin(void* ptr, int64_t nbytes, int* was_pinned);
+int btd_host_unpin(void* ptr);
+int btd_host_alloc(int64_t nbytes, void** out);
+int btd_host_free(void* ptr);
+
 /* Kernel launches issued by this library since load (the bench's
  * gpu_launches evidence) and the last error text. */
 int64_t btd_launch_count(void);

@@ -51,6 +51,10 @@ EXPORTS = (
     "btd_plan_set_profiling",
     "btd_plan_phase_times",
     "btd_copy_columns",
+    "btd_host_pin",
+    "btd_host_unpin",
+    "btd_host_alloc",
+    "btd_host_free",
     "btd_launch_count",
     "btd_last_error",
     "btd_version",
@@ -126,6 +130,14 @@ def load():
     lib.btd_plan_phase_times.restype = i32
     lib.btd_copy_columns.argtypes = [dp, i64, i64, i64, i64, dp, i32, vp]
     lib.btd_copy_columns.restype = i32
+    lib.btd_host_pin.argtypes = [vp, i64, ctypes.POINTER(i32)]
+    lib.btd_host_pin.restype = i32
+    lib.btd_host_unpin.argtypes = [vp]
+    lib.btd_host_unpin.restype = i32
+    lib.btd_host_alloc.argtypes = [i64, ctypes.POINTER(vp)]
+    lib.btd_host_alloc.restype = i32
+    lib.btd_host_free.argtypes = [vp]
+    lib.btd_host_free.restype = i32
     lib.btd_launch_count.argtypes = []
     lib.btd_launch_count.restype = i64
     lib.btd_last_error.argtypes = []

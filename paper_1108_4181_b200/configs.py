@@ -81,6 +81,43 @@ def strip_torch(n, m, k, shift=0.01, seed=0, device="cuda"):
     return diag, eye, eye.clone(), f
 
 
+def _normal_rows(rng, n, m, k, cols, chunk_rows):
+    """Columns ``cols`` of ``rng.standard_normal((n, m, k))`` drawn in row chunks:
+    Generator draws are sequential, so chunked draws give the identical stream."""
+    cols = np.asarray(cols, dtype=np.int64)
+    out = np.empty((n, m, len(cols)))
+    for r0 in range(0, n, chunk_rows):
+        r1 = min(n, r0 + chunk_rows)
+        out[r0:r1] = rng.standard_normal(size=(r1 - r0, m, k))[:, :, cols]
+    return out
+
+
+def generate_columns(name, cols, *, seed=0, chunk_rows=None):
+    """Numpy-stream inputs of config ``name`` with F restricted to columns ``cols``.
+
+    (diag, lower, upper, F[:, :, cols]) are bit-identical to ``generate(name)``
+    (same generator, same draw order), without holding the full F: this is how
+    the full-size parity tests and the reference-written full-size goldens
+    (tests/golden/make_fullsize_golden.py) get identical inputs at BASELINE sizes."""
+    cfg = dict(CONFIGS[name])
+    n, m, k = cfg["n"], cfg["m"], cfg["k"]
+    if chunk_rows is None:
+        chunk_rows = max(1, (1 << 24) // (m * k))
+    if cfg["kind"] == "dominant":
+        rng = np.random.default_rng(seed)
+        s = 1.0 / (4 * m)
+        lower = rng.uniform(-1.0, 1.0, size=(n - 1, m, m)) * s
+        upper = rng.uniform(-1.0, 1.0, size=(n - 1, m, m)) * s
+        diag = rng.uniform(-1.0, 1.0, size=(n, m, m)) * s
+        diag += np.eye(m)
+        return diag, lower, upper, _normal_rows(rng, n, m, k, cols, chunk_rows)
+    if cfg["kind"] == "strip":
+        diag, lower, upper, _ = strip_numpy(n, m, 0, cfg["shift"], seed)
+        return diag, lower, upper, _normal_rows(np.random.default_rng(seed), n, m, k, cols, chunk_rows)
+    d, lo, up, f = generate(name, seed=seed)
+    return d, lo, up, np.ascontiguousarray(f[:, :, np.asarray(cols)])
+
+
 def generate(name, *, device=None, seed=0, n=None, k=None):
     """Inputs of config ``name`` (optionally with N or K overridden)."""
     cfg = dict(CONFIGS[name])

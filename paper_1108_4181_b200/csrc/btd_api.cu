@@ -2152,6 +2152,54 @@ int btd_copy_columns(double* host, int64_t rows, int64_t K, int64_t c0, int64_t 
   }
   return BTD_OK;
 }
+int btd_host_pin(void* ptr, int64_t nbytes, int* was_pinned) {
+  if (was_pinned) *was_pinned = 0;
+  if (!ptr || nbytes < 0) { g_err = "btd_host_pin: bad arguments"; return BTD_ERR_INVALID_ARG; }
+  if (nbytes == 0) return BTD_OK;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) == cudaSuccess && a.type == cudaMemoryTypeHost) {
+    if (was_pinned) *was_pinned = 1;
+    return BTD_OK;
+  }
+  cudaGetLastError();
+  const cudaError_t e = cudaHostRegister(ptr, (size_t)nbytes, cudaHostRegisterDefault);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    cudaGetLastError();
+    if (was_pinned) *was_pinned = 1;
+    return BTD_OK;
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    g_err = std::string("btd_host_pin: ") + cudaGetErrorString(e);
+    return BTD_ERR_CUDA;
+  }
+  return BTD_OK;
+}
+int btd_host_unpin(void* ptr) {
+  if (!ptr) return BTD_ERR_INVALID_ARG;
+  const cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    g_err = std::string("btd_host_unpin: ") + cudaGetErrorString(e);
+    return BTD_ERR_CUDA;
+  }
+  return BTD_OK;
+}
+int btd_host_alloc(int64_t nbytes, void** out) {
+  if (!out || nbytes < 1) { g_err = "btd_host_alloc: bad arguments"; return BTD_ERR_INVALID_ARG; }
+  const cudaError_t e = cudaHostAlloc(out, (size_t)nbytes, cudaHostAllocDefault);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *out = nullptr;
+    g_err = std::string("btd_host_alloc: ") + cudaGetErrorString(e);
+    return BTD_ERR_OOM;
+  }
+  return BTD_OK;
+}
+int btd_host_free(void* ptr) {
+  if (!ptr) return BTD_OK;
+  return cudaFreeHost(ptr) == cudaSuccess ? BTD_OK : BTD_ERR_CUDA;
+}
 int64_t btd_launch_count(void) { return g_launches.load(); }
 const char* btd_last_error(void) { return g_err.c_str(); }
 

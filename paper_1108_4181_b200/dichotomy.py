@@ -109,6 +109,18 @@ class DevicePlan:
     def matches(self, matrix) -> bool:
         return matrix.fingerprint() == self.matrix_fingerprint
 
+    # host-side internals of the reference DichotomyPlan (dichotomy.py:99-131) that
+    # its harness / io read; a GPU plan keeps their equivalents in HBM
+    _REF_INTERNALS = ("padded", "ranges", "reduced", "tree", "inverse_rows")
+
+    def __getattr__(self, name):
+        if name in DevicePlan._REF_INTERNALS:
+            raise AttributeError(
+                f"DevicePlan has no host '{name}': its factors live in HBM. Solve with plan_solve; after "
+                "install.install() the reference's harness.harness_solve and io.write_plan/read_plan "
+                "accept GPU plans")
+        raise AttributeError(name)
+
     def close(self):
         if getattr(self, "_h", None):
             _native.load().btd_plan_destroy(self._h)
@@ -199,11 +211,99 @@ def _solve_tensor(plan, f):
     return x.squeeze(2) if squeeze else x
 
 
+# ---- host memory for the numpy path ------------------------------------------
+# The reference's plan_solve takes and returns numpy arrays (dichotomy.py:358-390).
+# The library's host pipeline (btd_plan_solve_host) overlaps H2D, solve and D2H
+# only on page-locked memory, so large host solves
+#   * page-lock the caller's input buffer once (cudaHostRegister through
+#     btd_host_pin), for the lifetime of the array that owns it -- a repeated
+#     solve of the same batch pays nothing;
+#   * return their solution in a page-locked array drawn from a small pool
+#     (btd_host_alloc); the block goes back to the pool when the array dies.
+# Small batches are latency-bound and take the plain path.
+PIN_MIN_BYTES = 32 << 20
+_POOL_KEEP = 2            # free blocks kept per size
+_pinned_owners = {}       # id(owner) -> weakref.finalize
+_pool = {}                # nbytes -> [ptr, ...]
+
+
+class _PinnedBlock:
+    __slots__ = ("ptr", "nbytes", "__weakref__")
+
+    def __init__(self, nbytes):
+        ptr = ctypes.c_void_p()
+        _native.check(_native.load().btd_host_alloc(nbytes, ctypes.byref(ptr)))
+        self.ptr, self.nbytes = ptr.value, nbytes
+
+    def __del__(self):  # back to the pool (or freed past the pool's depth)
+        try:
+            free = _pool.setdefault(self.nbytes, [])
+            if len(free) < _POOL_KEEP:
+                free.append(self.ptr)
+            else:
+                _native.load().btd_host_free(ctypes.c_void_p(self.ptr))
+        except Exception:  # pragma: no cover - interpreter teardown
+            pass
+
+
+def _pinned_empty(shape):
+    """Uninitialised float64 C-contiguous array in page-locked memory."""
+    count = int(np.prod(shape))
+    nbytes = count * 8
+    free = _pool.get(nbytes)
+    if free:
+        blk = _PinnedBlock.__new__(_PinnedBlock)
+        blk.ptr, blk.nbytes = free.pop(), nbytes
+    else:
+        blk = _PinnedBlock(nbytes)
+    buf = (ctypes.c_double * count).from_address(blk.ptr)
+    buf._owner = blk
+    return np.frombuffer(buf, dtype=np.float64).reshape(shape)
+
+
+def _unpin(ptr):
+    try:
+        _native.load().btd_host_unpin(ctypes.c_void_p(ptr))
+    except Exception:  # pragma: no cover - interpreter teardown
+        pass
+
+
+def _pin_input(a):
+    """Page-lock the buffer behind ``a`` until the array owning it is collected."""
+    import weakref
+
+    owner = a
+    while isinstance(owner.base, np.ndarray):
+        owner = owner.base
+    if not (owner.flags.c_contiguous and owner.flags.owndata) or owner.nbytes < PIN_MIN_BYTES:
+        return
+    key = id(owner)
+    fin = _pinned_owners.get(key)
+    if fin is not None and fin.alive:
+        return
+    was = ctypes.c_int(0)
+    st = _native.load().btd_host_pin(ctypes.c_void_p(owner.ctypes.data), owner.nbytes, ctypes.byref(was))
+    if st != _native.BTD_OK or was.value:
+        return  # already page-locked (e.g. a pinned torch tensor's view), or not lockable: plain copies
+
+    def drop(k=key, ptr=owner.ctypes.data):
+        _pinned_owners.pop(k, None)
+        _unpin(ptr)
+
+    _pinned_owners[key] = weakref.finalize(owner, drop)
+
+
 def _solve_host(plan, data):
     squeeze = data.ndim == 2
     fk = data[:, :, None] if squeeze else data
     fk = np.ascontiguousarray(fk, dtype=np.float64)
-    x = np.empty_like(fk)
+    big = fk.nbytes >= PIN_MIN_BYTES
+    if big and np.may_share_memory(fk, data):  # never lock a temporary converted copy
+        _pin_input(fk)
+    if big:
+        x = _pinned_empty(fk.shape)
+    else:
+        x = np.empty_like(fk)
     t = _torch()
     with t.cuda.device(plan.device):
         stream = _current_stream(plan.device)

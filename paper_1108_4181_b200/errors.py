@@ -70,6 +70,14 @@ class BlockTooSmall(BlocktriError):
     """Block order smaller than the band half-width (ref errors.py:64)."""
 
 
+class ConfigError(BlocktriError):
+    """Invalid CLI configuration (ref errors.py:84)."""
+
+
+class FileFormatError(BlocktriError):
+    """Malformed binary container (ref errors.py:88)."""
+
+
 class DeviceError(BlocktriError):
     """CUDA / NCCL failure or missing native library (no reference analogue:
     the reference never leaves the host)."""
@@ -79,11 +87,13 @@ _BY_NAME = {
     c.__name__: c
     for c in (BlocktriError, DimensionMismatch, SingularBlock, SingularPivot,
               IndexOutOfRange, InvalidRankCount, InconsistentRanges, DeadlockDetected,
-              StageViolation, Breakdown, UnlabeledNode, SubdomainSolveFailure, BandTooWide, BlockTooSmall, DeviceError)
+              StageViolation, Breakdown, UnlabeledNode, SubdomainSolveFailure, BandTooWide, BlockTooSmall,
+              ConfigError, FileFormatError, DeviceError)
 }
 
 
 _ORIGINAL = dict(_BY_NAME)
+_REPARENTED = {}
 
 
 def restore() -> None:
@@ -93,13 +103,27 @@ def restore() -> None:
 
 
 def rebind(module) -> None:
-    """Use another module's same-named exception classes (e.g. blocktri.errors)."""
+    """Use another module's same-named exception classes (e.g. blocktri.errors).
+
+    Names the other module lacks (``DeviceError``: the reference never leaves
+    the host) are re-created under that module's ``BlocktriError``, so one
+    ``except blocktri.errors.BlocktriError`` catches every failure of the path.
+    Code must therefore look classes up through this module at raise time
+    (``errors.X`` / :func:`get`), never bind them at import."""
     g = globals()
+    root = getattr(module, "BlocktriError", None)
     for name in list(_BY_NAME):
         cls = getattr(module, name, None)
         if isinstance(cls, type) and issubclass(cls, Exception):
             g[name] = cls
             _BY_NAME[name] = cls
+        elif isinstance(root, type) and issubclass(root, Exception):
+            key = (name, root)
+            if key not in _REPARENTED:
+                orig = _ORIGINAL[name]
+                _REPARENTED[key] = type(name, (root, orig), {"__module__": __name__, "__doc__": orig.__doc__})
+            g[name] = _REPARENTED[key]
+            _BY_NAME[name] = _REPARENTED[key]
 
 
 def get(name):

@@ -15,12 +15,16 @@ import tempfile
 
 import numpy as np
 
+from . import errors as _err
 from .core import BlockTriMatrix, BlockVector
-from .errors import BlocktriError
 
 
-class FileFormatError(BlocktriError):
-    """Malformed binary container (ref errors.py:84-85)."""
+def __getattr__(name):
+    # io.FileFormatError is errors.FileFormatError as currently bound (the
+    # reference's own class after install(), ref errors.py:88)
+    if name == "FileFormatError":
+        return _err.FileFormatError
+    raise AttributeError(name)
 
 
 def atomic_write(path, data: bytes):
@@ -39,14 +43,14 @@ def atomic_write(path, data: bytes):
 def _take(fh, nbytes, what):
     buf = fh.read(nbytes)
     if len(buf) != nbytes:
-        raise FileFormatError(f"truncated file while reading {what}")
+        raise _err.FileFormatError(f"truncated file while reading {what}")
     return buf
 
 
 def _header(fh, magic):
     got = fh.read(4)
     if got != magic:
-        raise FileFormatError(f"bad magic {got!r}, expected {magic!r}")
+        raise _err.FileFormatError(f"bad magic {got!r}, expected {magic!r}")
     return struct.unpack("<QQ", _take(fh, 16, "header"))
 
 
@@ -67,7 +71,7 @@ def read_matrix(path) -> BlockTriMatrix:
         lower = _f64(fh, (n - 1) * m * m, "lower blocks").reshape(n - 1, m, m)
         upper = _f64(fh, (n - 1) * m * m, "upper blocks").reshape(n - 1, m, m)
         if fh.read(1):
-            raise FileFormatError("trailing bytes after BTR1 payload")
+            raise _err.FileFormatError("trailing bytes after BTR1 payload")
     return BlockTriMatrix(diag, lower, upper)
 
 
@@ -82,7 +86,7 @@ def read_vector(path) -> BlockVector:
         n, m = _header(fh, b"BVC1")
         data = _f64(fh, n * m, "vector payload").reshape(n, m)
         if fh.read(1):
-            raise FileFormatError("trailing bytes after BVC1 payload")
+            raise _err.FileFormatError("trailing bytes after BVC1 payload")
     return BlockVector(data)
 
 
@@ -138,7 +142,7 @@ def _ref_plan_payload_bytes(n, m, ranks, L):
     return size
 
 
-def read_plan(path, matrix, *, device=None):
+def read_plan(path, matrix, *, device=None, split=1):
     """Load a DPLN plan and bind it to ``matrix`` (fingerprint-checked, ref io.py:149-203).
 
     GPU plan files are imported onto ``device`` without redoing the preprocessing.
@@ -150,37 +154,37 @@ def read_plan(path, matrix, *, device=None):
 
     with open(path, "rb") as fh:
         if fh.read(4) != b"DPLN":
-            raise FileFormatError("bad magic, expected b'DPLN'")
+            raise _err.FileFormatError("bad magic, expected b'DPLN'")
         (version,) = struct.unpack("<Q", _take(fh, 8, "version"))
         if version not in (REF_PLAN_VERSION, GPU_PLAN_VERSION):
-            raise FileFormatError(f"unsupported plan version {version}")
+            raise _err.FileFormatError(f"unsupported plan version {version}")
         n, m, ranks, L, npad = struct.unpack("<QQQQQ", _take(fh, 40, "plan dims"))
         (fplen,) = struct.unpack("<Q", _take(fh, 8, "fingerprint length"))
         fingerprint = _take(fh, fplen, "fingerprint").decode("ascii")
         if matrix.fingerprint() != fingerprint:
-            raise FileFormatError("plan does not belong to this matrix")
+            raise _err.FileFormatError("plan does not belong to this matrix")
         if matrix.n != n or matrix.m != m:
-            raise FileFormatError("plan dimensions disagree with the matrix")
+            raise _err.FileFormatError("plan dimensions disagree with the matrix")
         if version == REF_PLAN_VERSION:
             body = fh.seek(0, os.SEEK_END) - (4 + 8 + 40 + 8 + fplen)
             if body != _ref_plan_payload_bytes(n, m, ranks, L):
-                raise FileFormatError("DPLN payload length does not match its header")
-            return dichotomy.plan_build(matrix, ranks, device=device)
+                raise _err.FileFormatError("DPLN payload length does not match its header")
+            return dichotomy.plan_build(matrix, ranks, split=split, device=device)
         split, nbytes = struct.unpack("<QQ", _take(fh, 16, "image header"))
         image = np.fromfile(fh, dtype=np.uint8, count=nbytes)
         if image.size != nbytes:
-            raise FileFormatError("truncated file while reading plan image")
+            raise _err.FileFormatError("truncated file while reading plan image")
         if fh.read(1):
-            raise FileFormatError("trailing bytes after DPLN payload")
+            raise _err.FileFormatError("trailing bytes after DPLN payload")
     lib = _native.load()
     dev = dichotomy._resolve_device(device)
     handle = ctypes.c_void_p()
     status = lib.btd_plan_import(ctypes.c_void_p(image.ctypes.data), int(nbytes), dev, None, ctypes.byref(handle))
     if status == _native.BTD_ERR_INVALID_ARG or status == _native.BTD_ERR_UNSUPPORTED:
-        raise FileFormatError(f"plan image rejected: {_native.last_error()}")
+        raise _err.FileFormatError(f"plan image rejected: {_native.last_error()}")
     _native.check(status)
     plan = dichotomy.DevicePlan(handle, n, m, int(ranks), int(split), dev, fingerprint)
     if plan.L != L or plan.npad != npad:
         plan.close()
-        raise FileFormatError("plan image disagrees with its DPLN header")
+        raise _err.FileFormatError("plan image disagrees with its DPLN header")
     return plan

@@ -1,5 +1,6 @@
 """bench.py pieces that run without a GPU: the reference arm's single JSON line
-(C port of the reference algorithm on the host cores) and the plan-parameter
+(the unmodified reference's plan_solve from oracle/_ref on the host cores; the
+C port of its algorithm when the reference is not built) and the plan-parameter
 policy behind every bench line (whole waves of sweep CTAs per GPU)."""
 import json
 import os
@@ -22,7 +23,11 @@ def test_reference_arm_prints_one_json_line():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["unit"] == "RHS/s" and d["value"] > 0
     assert d["e2e"] == {"value": d["value"], "unit": "RHS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refcpu
+
+    assert d["cpu_baseline"]["kind"] == ("reference" if refcpu.available() else "port")
+    assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["value"] == d["value"]
     assert d["config"]["workload"] == "c0" and d["steps"] == 2 and d["warmup"] == 1
 
 
