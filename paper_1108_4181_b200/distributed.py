@@ -102,6 +102,21 @@ class NativeBackend:
     def empty(self, nel):
         return self.torch.empty(nel, dtype=self.torch.float64, device=f"cuda:{self.device}")
 
+    def prepare(self, f, out):
+        """f as a contiguous float64 tensor on this device (converted if needed);
+        ``out`` must already be one of f's shape -- the C side has no sizes."""
+        t = self.torch
+        dev = t.device("cuda", self.device)
+        if not isinstance(f, t.Tensor):
+            f = t.as_tensor(np.asarray(f, dtype=np.float64))
+        f = f.to(device=dev, dtype=t.float64).contiguous()
+        if out is None:
+            return f, t.empty_like(f)
+        if (not isinstance(out, t.Tensor) or out.device != dev or out.dtype != t.float64
+                or not out.is_contiguous() or tuple(out.shape) != tuple(f.shape)):
+            raise _err.DimensionMismatch(f"out must be a contiguous float64 tensor of shape {tuple(f.shape)} on {dev}")
+        return f, out
+
     def exchange_size(self, h, k):
         nc, npart = ctypes.c_int64(), ctypes.c_int64()
         _native.check(self.lib.btd_shard_exchange_size(h, k, ctypes.byref(nc), ctypes.byref(npart)))
@@ -166,6 +181,8 @@ class ShardedPlan:
         st, row = backend.finish(h, allc)
         if st:
             msg = _native.last_error() if isinstance(backend, NativeBackend) else "singular reduced system"
+            backend.destroy(h)  # no plan object will own the handle
+            self.h = None
             if st == _native.BTD_ERR_SINGULAR_PIVOT:
                 raise _err.SingularPivot(row, msg)
             _native.check(st, row)
@@ -225,8 +242,19 @@ class ShardedPlan:
         (written into ``out`` when given; may alias f_local).  ``trace``: an
         :class:`~.trace.ExecutionTrace` (nranks = world) that receives the logical
         stages and measured times of the two exchanges."""
+        rows = self.row_hi - self.row_lo
+        if len(f_local.shape) != 3 or tuple(int(v) for v in f_local.shape[:2]) != (rows, self.m):
+            raise _err.DimensionMismatch(
+                f"shard rhs must be ({rows}, {self.m}, k) (rows {self.row_lo}..{self.row_hi}), "
+                f"got {tuple(f_local.shape)}")
         k = int(f_local.shape[2])
-        x_local = f_local.new_empty(f_local.shape) if out is None else out
+        if k < 1:
+            raise _err.empty_rhs("right-hand-side batch with zero columns")
+        prep = getattr(self.be, "prepare", None)
+        if prep is not None:
+            f_local, x_local = prep(f_local, out)
+        else:
+            x_local = f_local.new_empty(f_local.shape) if out is None else out
         nc, npart = self.be.exchange_size(self.h, k)
         cap = (self.m * self.m + self.m) * 8 * k  # ref harness.py:166-180 message cap
         carry = self.be.empty(nc)
@@ -249,6 +277,13 @@ class ShardedPlan:
         c's solve (the sharded counterpart of ``btd_plan_solve_host``).  f_host /
         x_host: pinned CPU tensors (row_hi - row_lo, m, K); returns x_host."""
         torch = self.be.torch
+        shape = (self.row_hi - self.row_lo, self.m)
+        for nm, t in (("f_host", f_host), ("x_host", x_host)):
+            if (not isinstance(t, torch.Tensor) or t.device.type != "cpu" or t.dtype != torch.float64
+                    or not t.is_contiguous() or t.dim() != 3 or tuple(t.shape[:2]) != shape):
+                raise _err.DimensionMismatch(f"{nm} must be a contiguous float64 CPU tensor ({shape[0]}, {shape[1]}, k)")
+        if tuple(x_host.shape) != tuple(f_host.shape):
+            raise _err.DimensionMismatch("x_host must have f_host's shape")
         rows, m, k = (int(v) for v in f_host.shape)
         if chunks is None:  # as btd_plan_solve_host: >= 256-byte rows (64 columns from K = 256), <= 8
             chunks = max(1, min(8, k // (64 if k >= 256 else 32)))
@@ -256,10 +291,10 @@ class ShardedPlan:
         while k % nch or ((k // nch) % 2 and nch > 1):
             nch -= 1
         kc = k // nch
-        dev = torch.device("cuda", torch.cuda.current_device())
-        comp = torch.cuda.current_stream()
+        dev = torch.device("cuda", self.be.device)
+        comp = torch.cuda.current_stream(dev)
         if not hasattr(self, "_hstreams"):
-            self._hstreams = (torch.cuda.Stream(), torch.cuda.Stream())
+            self._hstreams = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
         s_in, s_out = self._hstreams
         nbuf = min(nch, 3)
         bufs = [torch.empty((rows, m, kc), dtype=torch.float64, device=dev) for _ in range(nbuf)]

@@ -152,11 +152,21 @@ def cg_solve(apply_op, rhs, precond=None, tol=1e-8, maxit=None, *, device=None):
 
 
 def gmres_solve(apply_op, rhs, precond=None, tol=1e-8, restart=None, maxit=None, *, device=None):
-    """Restarted GMRES on device vectors, left-preconditioned, CGS2 Arnoldi.
+    """Restarted, left-preconditioned GMRES on device vectors with the stopping
+    semantics of the reference's call ``scipy.sparse.linalg.gmres(rtol=tol,
+    atol=0, restart, maxiter, M, callback_type="pr_norm")`` (ref
+    schur.py:349-358; SciPy's published algorithm, restated):
 
-    Stops when the preconditioned residual estimate ||M(b - Ax)|| / ||M b|| <= tol;
-    ``maxit`` counts restart cycles.  Returns (x, converged, history) with the
-    per-iteration preconditioned residual estimates."""
+    * converged iff the TRUE residual ||b - A x|| <= tol ||b|| after a cycle;
+    * inside a cycle (modified Gram-Schmidt Arnoldi on M A, Givens QR) the
+      preconditioned residual estimate |g_{j+1}| stops the cycle once it is
+      <= ptol, where ptol starts at ||M b|| min(1, atol/||b||) and adapts after
+      every cycle from the true residual (tightened 4x when the estimate passed
+      but the true residual did not, loosened 1.5x otherwise);
+    * ``maxit`` counts restart cycles; ``history`` holds |g_{j+1}| / ||b|| per
+      inner iteration (the reference's "pr_norm" callback values).
+
+    Returns (x, converged, history)."""
     t = _device()
     dev = _resolve_device(device) if not isinstance(rhs, t.Tensor) else rhs.device.index
     b, was_np = _to_dev(rhs, dev)
@@ -166,50 +176,66 @@ def gmres_solve(apply_op, rhs, precond=None, tol=1e-8, restart=None, maxit=None,
     maxit = n if maxit is None else maxit
     M = precond if precond is not None else (lambda v: v)
     x = t.zeros_like(b)
-    bn = float(t.linalg.vector_norm(M(b)))
     history = []
-    if bn == 0.0:
+    bnrm = float(t.linalg.vector_norm(b))
+    if bnrm == 0.0:
         return _back(x, was_np), True, history
+    eps = np.finfo(np.float64).eps
+    atol = tol * bnrm
+    ptol_max = 1.0
+    ptol = float(t.linalg.vector_norm(M(b))) * min(1.0, atol / bnrm)
+    r = b.clone()
+    rnorm = bnrm
     for _cycle in range(maxit):
-        r = M(b - apply_op(x))
-        beta = float(t.linalg.vector_norm(r))
-        if beta / bn <= tol:
-            return _back(x, was_np), True, history
+        v0 = M(r)
+        beta = float(t.linalg.vector_norm(v0))
         V = t.zeros((restart + 1, n), dtype=t.float64, device=b.device)
-        V[0] = r / beta
+        V[0] = v0 / beta
         H = np.zeros((restart + 1, restart))
         cs, sn = np.zeros(restart), np.zeros(restart)
         g = np.zeros(restart + 1)
         g[0] = beta
+        breakdown = False
         j_done = 0
+        presid = beta
         for j in range(restart):
             w = M(apply_op(V[j]))
-            h = V[: j + 1] @ w
-            w = w - V[: j + 1].T @ h
-            h2 = V[: j + 1] @ w  # second pass (CGS2)
-            w = w - V[: j + 1].T @ h2
-            hcol = (h + h2).cpu().numpy()
+            h0 = float(t.linalg.vector_norm(w))
+            for i in range(j + 1):  # modified Gram-Schmidt
+                hij = float(t.dot(V[i], w))
+                H[i, j] = hij
+                w = w - hij * V[i]
             hn = float(t.linalg.vector_norm(w))
-            H[: j + 1, j] = hcol
             H[j + 1, j] = hn
-            if hn > 0:
+            if hn <= eps * h0:  # exact-solution indicator
+                H[j + 1, j] = 0.0
+                breakdown = True
+            else:
                 V[j + 1] = w / hn
-            for i in range(j):  # apply the previous Givens rotations
-                a, c = H[i, j], H[i + 1, j]
-                H[i, j], H[i + 1, j] = cs[i] * a + sn[i] * c, -sn[i] * a + cs[i] * c
+            for i in range(j):  # previous Givens rotations
+                a_, c_ = H[i, j], H[i + 1, j]
+                H[i, j], H[i + 1, j] = cs[i] * a_ + sn[i] * c_, -sn[i] * a_ + cs[i] * c_
             den = math.hypot(H[j, j], H[j + 1, j])
             cs[j], sn[j] = (1.0, 0.0) if den == 0 else (H[j, j] / den, H[j + 1, j] / den)
             H[j, j], H[j + 1, j] = den, 0.0
             g[j + 1], g[j] = -sn[j] * g[j], cs[j] * g[j]
             j_done = j + 1
-            history.append(abs(g[j + 1]) / bn)
-            if history[-1] <= tol or hn == 0:
+            presid = abs(g[j + 1])
+            history.append(presid / bnrm)
+            if presid <= ptol or breakdown:
                 break
-        y = np.linalg.solve(np.triu(H[:j_done, :j_done]), g[:j_done]) if j_done else np.zeros(0)
+        y = np.linalg.lstsq(np.triu(H[:j_done, :j_done]), g[:j_done], rcond=None)[0] if j_done else np.zeros(0)
         x = x + V[:j_done].T @ t.from_numpy(y).to(b.device)
-        if history and history[-1] <= tol:
-            return _back(x, was_np), True, history
-    return _back(x, was_np), False, history
+        r = b - apply_op(x)
+        rnorm = float(t.linalg.vector_norm(r))
+        if rnorm <= atol or breakdown:
+            break
+        if presid <= ptol:
+            ptol_max = max(eps, 0.25 * ptol_max)
+        else:
+            ptol_max = min(1.0, 1.5 * ptol_max)
+        ptol = presid * min(ptol_max, atol / rnorm)
+    return _back(x, was_np), rnorm <= atol, history
 
 
 # ------------------------------------------------------------------- operators

@@ -11,13 +11,13 @@ import subprocess
 import sys
 import warnings
 
-from make_golden import HERE, SCRATCH, build_reference
+from make_golden import HERE, REPO
 
 
 def child():
     import numpy as np
 
-    sys.path.insert(0, str(SCRATCH / "src"))
+    sys.path.insert(0, str(REPO / "oracle" / "_ref"))
     sys.path.insert(0, str(HERE))
     from blocktri import core, schur
     from schur_cases import CASES, build
@@ -32,15 +32,19 @@ def child():
         arrays[f"{name}.x"] = x
         arrays[f"{name}.rhs"] = schur.schur_rhs(sys_, f)
         arrays[f"{name}.S_e0"] = schur.schur_apply(sys_, np.eye(sys_.ngamma)[0])
-        m = dict(iterations=st.iterations, relative_residual=st.relative_residual, converged=st.converged)
-        if symm:
-            with warnings.catch_warnings():
-                warnings.simplefilter("ignore")
-                pc, band = schur.probing_preconditioner(sys_, 2, ranks=2)
-            arrays[f"{name}.band"] = band.bands
-            xp, stp = schur.solve_schur(sys_, f, tol=1e-10, precond=pc.apply)
-            arrays[f"{name}.xp"] = xp
-            m.update(precond_iterations=stp.iterations, precond_fallback=bool(pc.fallback))
+        m = dict(iterations=st.iterations, relative_residual=st.relative_residual, converged=st.converged,
+                 history=[float(h) for h in st.history])
+        # probing preconditioner on every case; on the unsymmetric (PML-like) one it drives the
+        # preconditioned scipy GMRES the reference uses there (schur.py:349-358)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            pc, band = schur.probing_preconditioner(sys_, 2, ranks=2)
+        arrays[f"{name}.band"] = band.bands
+        xp, stp = schur.solve_schur(sys_, f, tol=1e-10, precond=pc.apply)
+        arrays[f"{name}.xp"] = xp
+        m.update(precond_iterations=stp.iterations, precond_fallback=bool(pc.fallback),
+                 precond_converged=bool(stp.converged), precond_relative_residual=stp.relative_residual,
+                 precond_history=[float(h) for h in stp.history])
         meta[name] = m
     np.savez_compressed(HERE / "schur_golden.npz", **arrays)
     (HERE / "schur_golden.json").write_text(json.dumps(meta, indent=1))
@@ -51,6 +55,6 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "--child":
         child()
     else:
-        build_reference()
+        subprocess.run([str(REPO / "oracle" / "build_ref.sh")], check=True)
         res = subprocess.run([sys.executable, __file__, "--child"], check=True, capture_output=True, text=True)
         print(res.stdout.strip())
