@@ -591,7 +591,8 @@ def run_b200(args):
                 plan.solve_host(Fp, Xp)
                 return Xp
             api = "ShardedPlan.solve_host(pinned host rows) (per-rank host pipeline)"
-        xh = solve_host()  # warm: pins F once, fills the pinned solution pool
+        for _ in range(2):  # warm: page-locks F once and fills the 2-deep pinned solution pool
+            xh = solve_host()
         del xh
         if dist:
             dist.barrier()

@@ -76,7 +76,13 @@ int btd_plan_create(const double* diag, const double* lower, const double* upper
 
 /* Algorithm 2 step 2 (ref dichotomy.py:358-390) on DEVICE buffers:
  * f, x are (n,m,k) float64 on the plan's device; x may alias f.
- * Stream-ordered; returns once enqueued.  No block factorization. */
+ * Stream-ordered; returns once enqueued.  No block factorization.
+ * Threading: the plan is read-only after creation and calls are thread-safe.
+ * Its solve scratch is shared, so solves on one plan issued on different
+ * streams are ordered on the device (the later call's stream waits on an event
+ * of the earlier one; the host never blocks).  Independent concurrent solves
+ * of one matrix use one plan per stream, or btd_plan_solve_host, which runs
+ * its column chunks on up to four internal streams at once. */
 int btd_plan_solve(btd_plan* plan, const double* f, double* x, int64_t k, void* stream);
 
 /* Same on HOST buffers (the reference's numpy-in / numpy-out contract): copies

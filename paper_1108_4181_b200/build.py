@@ -46,7 +46,7 @@ def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()
         return OUT
     os.makedirs(os.path.dirname(out), exist_ok=True)
     cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp",
-           os.path.join(CSRC, "btd_api.cu"), "-lcusolver", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+           os.path.join(CSRC, "btd_api.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -36,12 +36,12 @@
 #include <vector>
 
 #include <cudaTypedefs.h>
-#include <cusolverDn.h>
 
 #include "blocktri_b200.h"
 #include "btd_chain.cuh"
 #include "btd_gemm.cuh"
 #include "btd_inv.cuh"
+#include "btd_gjc.cuh"
 #include "btd_band.cuh"
 #include "btd_tree.cuh"
 
@@ -142,59 +142,6 @@ __global__ void assemble_rows_kernel(const double* Y, const int64_t* ynb0, const
 }
 
 // row-major D (mp x mp) -> col-major copy of D (i.e. row-major D^T)
-__global__ void transpose_one_kernel(const double* in, double* out, int mp) {
-  __shared__ double tile[32][33];
-  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
-  for (int i = threadIdx.y; i < 32; i += 8) {
-    const int r = by + i, c = bx + threadIdx.x;
-    tile[i][threadIdx.x] = (r < mp && c < mp) ? in[(int64_t)r * mp + c] : 0.0;
-  }
-  __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += 8) {
-    const int r = bx + i, c = by + threadIdx.x;
-    if (r < mp && c < mp) out[(int64_t)r * mp + c] = tile[threadIdx.x][i];
-  }
-}
-
-// Reference pivot test on an LU of D (ref _kernels.pyx:35-63): fail at the first
-// k < m with |U_kk| <= rcond * ||D[:m,:m]||_inf.  D row-major, LU col-major.
-__global__ void lu_pivot_check_kernel(const double* D, const double* LU, int m, int mp, double rcond, int step,
-                                      int32_t* fail_step, int32_t* fail_col, int64_t slot) {
-  __shared__ double red[32];
-  __shared__ int redk[32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  double mx = 0.0;
-  for (int r = warp; r < m; r += nw) {
-    double sum = 0.0;
-    for (int c = lane; c < m; c += 32) sum += fabs(D[(int64_t)r * mp + c]);
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    mx = fmax(mx, sum);
-  }
-  if (lane == 0) red[warp] = mx;
-  __syncthreads();
-  if (tid == 0) {
-    double t = 0.0;
-    for (int w = 0; w < nw; ++w) t = fmax(t, red[w]);
-    red[0] = t * rcond;
-  }
-  __syncthreads();
-  const double tol = red[0];
-  __syncthreads();
-  int kmin = m;
-  for (int k = tid; k < m; k += blockDim.x)
-    if (!(fabs(LU[(int64_t)k * mp + k]) > tol)) kmin = min(kmin, k);
-  for (int o = 16; o; o >>= 1) kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-  if (lane == 0) redk[warp] = kmin;
-  __syncthreads();
-  if (tid == 0) {
-    int k = m;
-    for (int w = 0; w < nw; ++w) k = min(k, redk[w]);
-    if (k < m && fail_step[slot] < 0) {
-      fail_step[slot] = step;
-      fail_col[slot] = k;
-    }
-  }
-}
 
 // cudaFuncSetAttribute is per device: remember which (kernel, device) pairs were set.
 void set_smem_attr(const void* fn, size_t smem) {
@@ -497,6 +444,7 @@ struct btd_plan {
   int64_t hostio_k = 0;
   std::mutex mu;
   cudaStream_t last_stream = nullptr;
+  cudaEvent_t ev_done = nullptr;  // recorded after every call on its stream (cross-stream ordering)
   int64_t factor_bytes = 0;
   // CUDA graphs of repeated solves: key (F, X, K) -> instantiated graph on the plan's stream
   struct GraphEntry {
@@ -516,9 +464,7 @@ struct btd_plan {
   DevBuf hchunk;  // kHostBufs x chunk elements
   int64_t hchunk_elems = 0;
   // cuSOLVER for block orders above 256 (preprocessing only)
-  cusolverDnHandle_t solver = nullptr;
-  DevBuf sv_work, sv_ipiv, sv_info, sv_lu;
-  int sv_lwork = 0;
+  DevBuf gjc_aux;  // blocked Gauss-Jordan (block orders other than 128/256 above 64): pivots, tol, dead flags
   // profiling: 4 events per solve (before fwd, after fwd, after tree, after bwd)
   bool profiling = false;
   std::vector<cudaEvent_t> ev_free, ev_pending;
@@ -550,7 +496,6 @@ struct btd_plan {
   ~btd_plan() {
     for (auto e : ev_pending) cudaEventDestroy(e);
     for (auto e : ev_free) cudaEventDestroy(e);
-    if (solver) cusolverDnDestroy(solver);
     for (auto& g : graphs)
       if (g.exec) cudaGraphExecDestroy(g.exec);
     for (auto& x : sc) {
@@ -562,6 +507,7 @@ struct btd_plan {
       if (x.ev_join) cudaEventDestroy(x.ev_join);
     }
     if (s_in) cudaStreamDestroy(s_in);
+    if (ev_done) cudaEventDestroy(ev_done);
     if (s_out) cudaStreamDestroy(s_out);
     for (auto x : s_c)
       if (x) cudaStreamDestroy(x);
@@ -599,54 +545,72 @@ void launch_inv(btd_plan& pl, int nbatch, const double* in, const int64_t* idx_i
                 int32_t* fail_col, DevBuf& ws, cudaStream_t st, const int64_t* fail_map = nullptr) {
   if (nbatch <= 0) return;
   const int mp = (int)pl.mp;
-  if (mp > 256) {
-    // cuSOLVER route: getrf on D (col-major view of D^T), reference pivot test on
-    // diag(U), getrs(transpose) against I -> D^{-1} written row-major.
-    auto host_idx = [&](const int64_t* di) {
-      std::vector<int64_t> h(nbatch);
-      if (di) {  // stream-ordered: the index arrays may still be in flight on st (StagedUploads)
-        CK(cudaMemcpyAsync(h.data(), di, sizeof(int64_t) * nbatch, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+  if (mp > 64) {
+    GjcDesc g{};
+    g.in = in; g.idx_in = idx_in; g.add_in = add_in;
+    g.out = out; g.idx_out = idx_out; g.add_out = add_out;
+    g.nbatch = nbatch; g.m = (int)pl.m; g.mp = mp;
+    g.step = step; g.active_until = nullptr;
+    g.fail_step = fail_step; g.fail_map = fail_map; g.fail_col = fail_col;
+    g.rcond = 1e-13;  // ref _kernels.pyx:19
+    if (mp == 128 || mp == 256) {
+      // one cluster of 8 CTAs per block holds all of [D | I] in shared memory
+      g.c0 = 0; g.k0 = 0; g.npiv = mp; g.full = 1;
+      if (mp == 256) {
+        const size_t smem = GjcSmem<64, 8>::bytes(mp);
+        set_smem_attr((const void*)gjc_panel_kernel<64, 8>, smem);
+        gjc_panel_kernel<64, 8><<<nbatch * 8, GJC_NT, smem, st>>>(g);
       } else {
-        for (int b = 0; b < nbatch; ++b) h[b] = b;
+        const size_t smem = GjcSmem<32, 8>::bytes(mp);
+        set_smem_attr((const void*)gjc_panel_kernel<32, 8>, smem);
+        gjc_panel_kernel<32, 8><<<nbatch * 8, GJC_NT, smem, st>>>(g);
       }
-      return h;
-    };
-    const std::vector<int64_t> hin = host_idx(idx_in), hout = host_idx(idx_out), hmap = host_idx(fail_map);
-    auto cs = [&](cusolverStatus_t e, const char* what) {
-      if (e != CUSOLVER_STATUS_SUCCESS) fail(BTD_ERR_CUDA, std::string("cuSOLVER failure: ") + what);
-    };
-    if (!pl.solver) cs(cusolverDnCreate(&pl.solver), "create");
-    cs(cusolverDnSetStream(pl.solver, st), "set stream");
-    const size_t bb = (size_t)mp * mp;
-    if (pl.sv_lu.bytes < bb * sizeof(double)) {
-      pl.sv_lu.alloc(bb * sizeof(double));
-      pl.sv_ipiv.alloc(sizeof(int) * mp);
-      pl.sv_info.alloc(sizeof(int));
-      int lw = 0;
-      cs(cusolverDnDgetrf_bufferSize(pl.solver, mp, mp, pl.sv_lu.d(), mp, &lw), "bufferSize");
-      pl.sv_lwork = lw;
-      pl.sv_work.alloc(sizeof(double) * std::max(lw, 1));
+      CK_LAUNCH();
+      return;
     }
-    for (int b = 0; b < nbatch; ++b) {
-      const double* D = in + (hin[b] + add_in) * (int64_t)bb;
-      double* O = out + (hout[b] + add_out) * (int64_t)bb;
-      dim3 tg((mp + 31) / 32, (mp + 31) / 32);
-      transpose_one_kernel<<<tg, dim3(32, 8), 0, st>>>(D, pl.sv_lu.d(), mp);
+    // blocked: [D | I] in a workspace, 32-column panels on a 4-CTA cluster, DMMA trailing updates
+    if (mp > GJC_MAXMP) fail(BTD_ERR_UNSUPPORTED, "block order above 4096");
+    constexpr int PW = 32;
+    const size_t wbytes = (size_t)mp * 2 * mp * sizeof(double);
+    const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)nbatch, (size_t)(8ull << 30) / wbytes));
+    if (ws.bytes < (size_t)chunk * wbytes) ws.alloc((size_t)chunk * wbytes);
+    const size_t aux = (size_t)chunk * (PW * sizeof(int32_t) + sizeof(double) + sizeof(int32_t)) + 64;
+    if (pl.gjc_aux.bytes < aux) pl.gjc_aux.alloc(aux);
+    const size_t smem = GjcSmem<8, 4>::bytes(mp);
+    set_smem_attr((const void*)gjc_panel_kernel<8, 4>, smem);
+    for (int b0 = 0; b0 < nbatch; b0 += chunk) {
+      GjcDesc c = g;
+      c.nbatch = std::min(chunk, nbatch - b0);
+      c.idx_in = idx_in ? idx_in + b0 : nullptr;
+      c.add_in = idx_in ? add_in : add_in + b0;
+      c.idx_out = idx_out ? idx_out + b0 : nullptr;
+      c.add_out = idx_out ? add_out : add_out + b0;
+      // fail_map entries are per batch entry: offset the map (or the identity) by b0
+      c.fail_map = fail_map ? fail_map + b0 : nullptr;
+      if (!fail_map && b0) {
+        c.fail_step = fail_step + b0;
+        c.fail_col = fail_col + b0;
+      }
+      c.W = ws.d();
+      c.tol = reinterpret_cast<double*>(pl.gjc_aux.p);
+      c.dead = reinterpret_cast<int32_t*>(c.tol + chunk);
+      c.piv = c.dead + chunk;
+      gjc_init_kernel<<<std::min(c.nbatch, 1184), 256, 0, st>>>(c);
       CK_LAUNCH();
-      cs(cusolverDnDgetrf(pl.solver, mp, mp, pl.sv_lu.d(), mp, pl.sv_work.d(), static_cast<int*>(pl.sv_ipiv.p),
-                          static_cast<int*>(pl.sv_info.p)),
-         "getrf");
-      lu_pivot_check_kernel<<<1, 512, 0, st>>>(D, pl.sv_lu.d(), (int)pl.m, mp, 1e-13, step, fail_step, fail_col,
-                                               hmap[b]);
+      c.full = 0;
+      for (int k0 = 0; k0 < mp; k0 += PW) {
+        c.c0 = k0; c.k0 = k0; c.npiv = std::min(PW, mp - k0);
+        gjc_panel_kernel<8, 4><<<c.nbatch * 4, GJC_NT, smem, st>>>(c);
+        CK_LAUNCH();
+        const int ntiles = (2 * mp - (k0 + PW) + 31) / 32;
+        if (ntiles > 0) {
+          gjc_update_kernel<PW><<<c.nbatch * ntiles, 256, 0, st>>>(c, ntiles);
+          CK_LAUNCH();
+        }
+      }
+      gjc_extract_kernel<<<1184, 256, 0, st>>>(c);
       CK_LAUNCH();
-      set_identity_kernel<<<256, 256, 0, st>>>(O, mp);
-      CK_LAUNCH();
-      cs(cusolverDnDgetrs(pl.solver, CUBLAS_OP_T, mp, mp, pl.sv_lu.d(), mp, static_cast<const int*>(pl.sv_ipiv.p), O,
-                          mp, static_cast<int*>(pl.sv_info.p)),
-         "getrs");
     }
-    (void)ws;
     return;
   }
   InvDesc d;
@@ -2013,9 +1977,13 @@ int guarded(btd_plan* pl, void* stream, const std::function<void(cudaStream_t)>&
     DeviceGuard dg(pl->device);
     std::lock_guard<std::mutex> lk(pl->mu);
     cudaStream_t st = (cudaStream_t)stream;
-    if (pl->last_stream != st && pl->sc[0].k) CK(cudaStreamSynchronize(pl->last_stream));
+    // The plan's scratch is shared by its solves: a call on another stream than the
+    // previous one is ordered after it ON THE DEVICE (event wait, no host block).
+    if (!pl->ev_done) CK(cudaEventCreateWithFlags(&pl->ev_done, cudaEventDisableTiming));
+    if (pl->last_stream != st && pl->sc[0].k) CK(cudaStreamWaitEvent(st, pl->ev_done, 0));
     pl->last_stream = st;
     fn(st);
+    CK(cudaEventRecord(pl->ev_done, st));
   } catch (const BtdError& e) {
     return e.code;
   }

@@ -214,12 +214,14 @@ def _solve_tensor(plan, f):
 # ---- host memory for the numpy path ------------------------------------------
 # The reference's plan_solve takes and returns numpy arrays (dichotomy.py:358-390).
 # The library's host pipeline (btd_plan_solve_host) overlaps H2D, solve and D2H
-# only on page-locked memory, so large host solves
-#   * page-lock the caller's input buffer once (cudaHostRegister through
-#     btd_host_pin), for the lifetime of the array that owns it -- a repeated
-#     solve of the same batch pays nothing;
+# only on page-locked memory (pageable 2-D copies run at 1.5-6.5 GB/s: a c4 solve
+# from pageable buffers takes ~6 s, measured), so large host solves
+#   * page-lock the caller's input buffer (cudaHostRegister via btd_host_pin) for
+#     the lifetime of the array that owns it -- a repeated solve of the same batch
+#     pays nothing more;
 #   * return their solution in a page-locked array drawn from a small pool
-#     (btd_host_alloc); the block goes back to the pool when the array dies.
+#     (btd_host_alloc); a block returns to the pool when its array dies (two per
+#     size: the caller's previous result + the next).
 # Small batches are latency-bound and take the plain path.
 PIN_MIN_BYTES = 32 << 20
 _POOL_KEEP = 2            # free blocks kept per size
@@ -269,41 +271,41 @@ def _unpin(ptr):
 
 
 def _pin_input(a):
-    """Page-lock the buffer behind ``a`` until the array owning it is collected."""
+    """Page-lock the buffer behind ``a`` until the array owning it is collected.
+    Returns True when the buffer is page-locked."""
     import weakref
 
     owner = a
     while isinstance(owner.base, np.ndarray):
         owner = owner.base
     if not (owner.flags.c_contiguous and owner.flags.owndata) or owner.nbytes < PIN_MIN_BYTES:
-        return
+        return False
     key = id(owner)
     fin = _pinned_owners.get(key)
     if fin is not None and fin.alive:
-        return
+        return True
     was = ctypes.c_int(0)
     st = _native.load().btd_host_pin(ctypes.c_void_p(owner.ctypes.data), owner.nbytes, ctypes.byref(was))
-    if st != _native.BTD_OK or was.value:
-        return  # already page-locked (e.g. a pinned torch tensor's view), or not lockable: plain copies
+    if st != _native.BTD_OK:
+        return False  # not lockable: plain copies
+    if was.value:
+        return True  # already page-locked (e.g. a pinned torch tensor's view)
 
     def drop(k=key, ptr=owner.ctypes.data):
         _pinned_owners.pop(k, None)
         _unpin(ptr)
 
     _pinned_owners[key] = weakref.finalize(owner, drop)
+    return True
 
 
 def _solve_host(plan, data):
     squeeze = data.ndim == 2
     fk = data[:, :, None] if squeeze else data
     fk = np.ascontiguousarray(fk, dtype=np.float64)
-    big = fk.nbytes >= PIN_MIN_BYTES
-    if big and np.may_share_memory(fk, data):  # never lock a temporary converted copy
-        _pin_input(fk)
-    if big:
-        x = _pinned_empty(fk.shape)
-    else:
-        x = np.empty_like(fk)
+    pinned = (fk.nbytes >= PIN_MIN_BYTES and np.may_share_memory(fk, data)  # never lock a temporary copy
+              and _pin_input(fk))
+    x = _pinned_empty(fk.shape) if pinned else np.empty_like(fk)
     t = _torch()
     with t.cuda.device(plan.device):
         stream = _current_stream(plan.device)

@@ -39,4 +39,4 @@ for i in range(2):
     _native.check(lib.btd_plan_solve_host(plan.handle, ctypes.c_void_p(F.ctypes.data), ctypes.c_void_p(x.ctypes.data),
                                           F.shape[2], None))
     print(f"{name} raw btd_plan_solve_host (pinned F, pinned X): {1e3 * (time.perf_counter() - t0):.1f} ms", flush=True)
-os.environ["BTD_HOST_TRACE"] = "1"
+# per-chunk timeline of one more raw call (BTD_HOST_TRACE is read once per process)
