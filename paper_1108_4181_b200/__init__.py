@@ -7,11 +7,11 @@ in ``include/blocktri_b200.h``.  See DESIGN.md.
 
 from . import errors
 from .core import BlockTriMatrix, BlockVector
-from .dichotomy import DevicePlan, plan_build, plan_build_arrays, plan_solve
+from .dichotomy import DevicePlan, pinned_array, pinned_empty, plan_build, plan_build_arrays, plan_solve
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "BlockTriMatrix", "BlockVector", "DevicePlan", "errors", "plan_build", "plan_build_arrays",
-    "plan_solve",
+    "BlockTriMatrix", "BlockVector", "DevicePlan", "errors", "pinned_array", "pinned_empty", "plan_build",
+    "plan_build_arrays", "plan_solve",
 ]

@@ -554,27 +554,28 @@ void launch_inv(btd_plan& pl, int nbatch, const double* in, const int64_t* idx_i
     g.fail_step = fail_step; g.fail_map = fail_map; g.fail_col = fail_col;
     g.rcond = 1e-13;  // ref _kernels.pyx:19
     if (mp == 128 || mp == 256) {
-      // one cluster of 8 CTAs per block holds all of [D | I] in shared memory
+      // one cluster of 8 CTAs per block holds all of D in shared memory (in-place GJ)
       g.c0 = 0; g.k0 = 0; g.npiv = mp; g.full = 1;
       if (mp == 256) {
-        const size_t smem = GjcSmem<64, 8>::bytes(mp);
-        set_smem_attr((const void*)gjc_panel_kernel<64, 8>, smem);
-        gjc_panel_kernel<64, 8><<<nbatch * 8, GJC_NT, smem, st>>>(g);
-      } else {
         const size_t smem = GjcSmem<32, 8>::bytes(mp);
         set_smem_attr((const void*)gjc_panel_kernel<32, 8>, smem);
         gjc_panel_kernel<32, 8><<<nbatch * 8, GJC_NT, smem, st>>>(g);
+      } else {
+        const size_t smem = GjcSmem<16, 8>::bytes(mp);
+        set_smem_attr((const void*)gjc_panel_kernel<16, 8>, smem);
+        gjc_panel_kernel<16, 8><<<nbatch * 8, GJC_NT, smem, st>>>(g);
       }
       CK_LAUNCH();
       return;
     }
-    // blocked: [D | I] in a workspace, 32-column panels on a 4-CTA cluster, DMMA trailing updates
+    // blocked: D inverted in place in a workspace, 32-column panels on a 4-CTA cluster,
+    // DMMA updates of the other columns
     if (mp > GJC_MAXMP) fail(BTD_ERR_UNSUPPORTED, "block order above 4096");
     constexpr int PW = 32;
-    const size_t wbytes = (size_t)mp * 2 * mp * sizeof(double);
+    const size_t wbytes = (size_t)mp * (mp + PW) * sizeof(double);
     const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)nbatch, (size_t)(8ull << 30) / wbytes));
     if (ws.bytes < (size_t)chunk * wbytes) ws.alloc((size_t)chunk * wbytes);
-    const size_t aux = (size_t)chunk * (PW * sizeof(int32_t) + sizeof(double) + sizeof(int32_t)) + 64;
+    const size_t aux = (size_t)chunk * (2 * (size_t)mp * sizeof(int32_t) + sizeof(unsigned long long) + sizeof(int32_t));
     if (pl.gjc_aux.bytes < aux) pl.gjc_aux.alloc(aux);
     const size_t smem = GjcSmem<8, 4>::bytes(mp);
     set_smem_attr((const void*)gjc_panel_kernel<8, 4>, smem);
@@ -592,22 +593,24 @@ void launch_inv(btd_plan& pl, int nbatch, const double* in, const int64_t* idx_i
         c.fail_col = fail_col + b0;
       }
       c.W = ws.d();
-      c.tol = reinterpret_cast<double*>(pl.gjc_aux.p);
-      c.dead = reinterpret_cast<int32_t*>(c.tol + chunk);
+      c.rsmax = reinterpret_cast<unsigned long long*>(pl.gjc_aux.p);
+      c.dead = reinterpret_cast<int32_t*>(c.rsmax + chunk);
       c.piv = c.dead + chunk;
-      gjc_init_kernel<<<std::min(c.nbatch, 1184), 256, 0, st>>>(c);
+      c.colmap = c.piv + (size_t)chunk * mp;
+      CK(cudaMemsetAsync(pl.gjc_aux.p, 0, (size_t)chunk * (sizeof(unsigned long long) + sizeof(int32_t)), st));
+      gjc_init_kernel<<<1184, 256, 0, st>>>(c);
       CK_LAUNCH();
       c.full = 0;
+      const int ntiles = (mp + 31) / 32;
       for (int k0 = 0; k0 < mp; k0 += PW) {
         c.c0 = k0; c.k0 = k0; c.npiv = std::min(PW, mp - k0);
         gjc_panel_kernel<8, 4><<<c.nbatch * 4, GJC_NT, smem, st>>>(c);
         CK_LAUNCH();
-        const int ntiles = (2 * mp - (k0 + PW) + 31) / 32;
-        if (ntiles > 0) {
-          gjc_update_kernel<PW><<<c.nbatch * ntiles, 256, 0, st>>>(c, ntiles);
-          CK_LAUNCH();
-        }
+        gjc_update_kernel<PW><<<c.nbatch * ntiles, 256, 0, st>>>(c, ntiles);
+        CK_LAUNCH();
       }
+      gjc_colmap_kernel<<<(c.nbatch + 127) / 128, 128, 0, st>>>(c);
+      CK_LAUNCH();
       gjc_extract_kernel<<<1184, 256, 0, st>>>(c);
       CK_LAUNCH();
     }
@@ -2293,7 +2296,24 @@ int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int6
     int64_t kc = k;
     for (int64_t nch = maxch; nch >= 2; --nch)
       if (k % nch == 0 && (k / nch) % 2 == 0 && k / nch >= minw) { kc = k / nch; break; }
-    const int64_t nch = k / kc, rows = pl->n * pl->m;
+    // Chunk widths.  The copy pipes idle for one chunk's H2D + solve at the start and
+    // one chunk's solve + D2H at the end, so the first and last chunks are half as
+    // wide when that keeps >= 256-byte row segments (narrower 2-D copies lose rate:
+    // tools/microbench/hostio.cu, profiles/r02_hostio.txt): c1 256 = 32+64+64+64+32.
+    std::vector<int64_t> widths;
+    {
+      static int halves = -1;
+      if (halves < 0) halves = getenv("BTD_HOST_HALF_ENDS") ? atoi(getenv("BTD_HOST_HALF_ENDS")) : 1;
+      const int64_t n0 = k / kc;
+      if (halves && n0 >= 2 && kc % 4 == 0 && kc / 2 >= 32 && pl->mode == 0) {
+        widths.push_back(kc / 2);
+        for (int64_t c = 1; c < n0; ++c) widths.push_back(kc);
+        widths.push_back(kc / 2);
+      } else {
+        widths.assign((size_t)n0, kc);
+      }
+    }
+    const int64_t nch = (int64_t)widths.size(), rows = pl->n * pl->m;
     const size_t celems = (size_t)rows * kc;
     // concurrent solves: not with the cooperative tree kernel (two partially-resident
     // cooperative grids could wait on each other) or while phase profiling (per-solve
@@ -2358,7 +2378,8 @@ int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int6
     int64_t col = 0;
     for (int64_t c = 0; c < nch; ++c) {
       const int b = (int)(c % nbuf), sl = (int)(c % nstr);
-      const size_t wbytes = (size_t)kc * sizeof(double);
+      const int64_t wc = widths[(size_t)c];
+      const size_t wbytes = (size_t)wc * sizeof(double);
       const cudaStream_t cst = cs[sl];
       double* dbuf = pl->hchunk.d() + (size_t)b * celems;
       cudaEvent_t in_done = pl->ev_h[b][0], comp_done = pl->ev_h[b][1], out_done = pl->ev_h[b][2];
@@ -2370,7 +2391,7 @@ int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int6
       CK(cudaStreamWaitEvent(cst, in_done, 0));
       pl->cur = sl;
       tmark(cst);
-      solve_graphed(*pl, dbuf, dbuf, kc, cst);
+      solve_graphed(*pl, dbuf, dbuf, wc, cst);
       CK(cudaEventRecord(comp_done, cst));
       tmark(cst);
       CK(cudaStreamWaitEvent(pl->s_out, comp_done, 0));
@@ -2378,7 +2399,7 @@ int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int6
       CK(cudaMemcpy2DAsync(x_host + col, hpitch, dbuf, wbytes, wbytes, rows, cudaMemcpyDeviceToHost, pl->s_out));
       CK(cudaEventRecord(out_done, pl->s_out));
       tmark(pl->s_out);
-      col += kc;
+      col += wc;
     }
     pl->cur = 0;
     CK(cudaStreamSynchronize(pl->s_out));
@@ -2391,7 +2412,7 @@ int btd_plan_solve_host(btd_plan* pl, const double* f_host, double* x_host, int6
       for (int64_t c = 0; c < nch; ++c) {
         for (int i = 0; i < 6; ++i) CK(cudaEventElapsedTime(&ms[i], tev[0], tev[1 + 6 * c + i]));
         fprintf(stderr, "  chunk %lld w=%lld  h2d %7.2f-%7.2f  solve %7.2f-%7.2f  d2h %7.2f-%7.2f\n", (long long)c,
-                (long long)kc, ms[0], ms[1], ms[2], ms[3], ms[4], ms[5]);
+                (long long)widths[(size_t)c], ms[0], ms[1], ms[2], ms[3], ms[4], ms[5]);
       }
       for (auto e : tev) cudaEventDestroy(e);
     }

@@ -19,12 +19,14 @@
 // Gauss-Jordan column g (g_k = 1/p, g_i = -f_i/p), so that after the panel the
 // panel holds T_K, the K-columns of the accumulated row transform T
 // (T Pi W_rest = X + (T_K - E) X[K], X = Pi W_rest; verified against numpy).
-//   * full mode (mp <= 256): the panel IS [D | I] (PW = 2 mp), loaded from D, and
-//     the right half is D^{-1} at the end -- one launch per batch of blocks;
-//   * panel mode (mp > 256): W lives in a global workspace; panels of PW = 32
-//     columns alternate with gjc_update_kernel, the trailing rank-32 update
-//     W_rest += (T_K - E) X[K] on the fp64 tensor cores (DMMA), after the panel's
-//     row swaps.
+//   * full mode (mp = 128 / 256): the panel IS D (PW = mp), in-place Gauss-Jordan;
+//     the slice then holds D^{-1} up to the column permutation of the row swaps,
+//     undone by the store -- one launch per batch of blocks;
+//   * panel mode (other orders > 64): W = D in a global workspace (in place, padded
+//     to mp + 32 columns); panels of PW = 32 columns alternate with
+//     gjc_update_kernel, the rank-32 update of every other column
+//     W_rest += (T_K - E) X[K] on the fp64 tensor cores (DMMA) after the panel's row
+//     swaps; gjc_extract_kernel undoes the column permutation.
 #pragma once
 #include <cooperative_groups.h>
 
@@ -35,9 +37,10 @@ namespace btd {
 struct GjcDesc {
   const double* in;  const int64_t* idx_in;  int64_t add_in;     // D blocks (mp x mp)
   double* out;       const int64_t* idx_out; int64_t add_out;    // D^{-1} blocks
-  double* W;                   // panel mode: [nbatch][mp][2 mp] workspace
-  int32_t* piv;                // panel mode: [nbatch][PW] pivot rows of the current panel
-  double* tol;                 // panel mode: [nbatch] singularity threshold
+  double* W;                   // panel mode: [nbatch][mp][mp + 32] workspace (D, inverted in place)
+  int32_t* piv;                // panel mode: [nbatch][mp] pivot row of every column
+  int32_t* colmap;             // panel mode: [nbatch][mp] output column of every W column
+  unsigned long long* rsmax;   // panel mode: [nbatch] max row abs sum (bits of a nonnegative double)
   int32_t* dead;               // panel mode: [nbatch] entry failed (skip the rest)
   int nbatch, m, mp;
   int c0, k0, npiv, full;      // panel columns [c0, c0+PW), pivots k0..k0+npiv-1
@@ -54,24 +57,28 @@ constexpr int GJC_NT = 256;
 template <int CW, int CS>
 struct GjcSmem {
   static size_t bytes(int mp) {
-    // W slice | fcol | 2 broadcast columns (+3 scalars each) | rk | ok | reductions
-    return sizeof(double) * ((size_t)mp * CW + mp + 2 * ((size_t)mp + 4) + 2 * CW + 2 * (GJC_NT / 32));
+    // W slice | fcol | 2 broadcast columns (+3 scalars each) | rk | ok | pivots + column map (ints)
+    return sizeof(double) * ((size_t)mp * CW + mp + 2 * ((size_t)mp + 4) + 2 * CW) + sizeof(int) * 2 * (size_t)mp;
   }
 };
 
+// Full mode: in-place Gauss-Jordan on D itself (PW = mp columns): after the last
+// pivot the slice holds D^{-1} with its columns permuted by the row swaps, which
+// the store undoes (the swaps, in reverse order, applied to the columns).
+// Panel mode: the pivot columns end up as T_K (see the file comment).
 template <int CW, int CS>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_kernel(GjcDesc d) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double sm[];
-  const int mp = d.mp, m = d.m, W2 = 2 * mp;
+  const int mp = d.mp, m = d.m, LDW = mp + 32;
   double* Wl = sm;                          // [mp][CW]
   double* fcol = Wl + (size_t)mp * CW;      // [mp]  swapped multipliers of this step
   double* bc = fcol + mp;                   // [2][mp + 4]: column, p, pv, fail
-  double* rk = bc + 2 * (mp + 4);           // [CW]
-  double* okr = rk + CW;                    // [CW]
-  double* redv = okr + CW;                  // [NT/32]
-  int* redi = reinterpret_cast<int*>(redv + GJC_NT / 32);
+  double* rk = bc + 2 * (mp + 4);           // [CW]  new pivot row
+  double* okr = rk + CW;                    // [CW]  old row k (moves to row p)
+  int* piv_s = reinterpret_cast<int*>(okr + CW);  // [mp] pivot row of every step (full mode)
+  int* dest = piv_s + mp;                   // [mp] output column of every global column
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rank = (int)cluster.block_rank();
   const int b = blockIdx.x / CS;
@@ -80,59 +87,54 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
   if (!full && d.dead[b]) return;  // uniform over the cluster
   const int colbase = d.c0 + rank * CW;  // first global W column of this CTA
   const double* A = full ? d.in + ((d.idx_in ? d.idx_in[b] : (int64_t)b) + d.add_in) * (int64_t)mp * mp : nullptr;
-  double* Wg = full ? nullptr : d.W + (int64_t)b * mp * W2;
+  double* Wg = full ? nullptr : d.W + (int64_t)b * mp * LDW;
 
-  // ---- load the slice; full mode also computes the singularity threshold
-  double rs_part = 0.0;  // unused in panel mode
   for (int e = tid; e < mp * CW; e += GJC_NT) {
     const int r = e / CW, c = e - r * CW, gc = colbase + c;
-    double v;
-    if (full) v = gc < mp ? A[(int64_t)r * mp + gc] : (gc - mp == r ? 1.0 : 0.0);
-    else v = Wg[(int64_t)r * W2 + gc];
-    Wl[e] = v;
+    Wl[e] = full ? A[(int64_t)r * mp + gc] : Wg[(int64_t)r * LDW + gc];
   }
   double tol;
   if (full) {
-    // row abs sums of the leading m x m block: each CTA sums its columns, the
-    // partials meet through DSMEM
+    // singularity threshold: max row abs sum of the leading m x m block; each CTA
+    // sums its columns, the partials meet through DSMEM
     __syncthreads();
     for (int r = tid; r < mp; r += GJC_NT) {
-      double s = 0.0;
+      double sacc = 0.0;
       for (int c = 0; c < CW; ++c)
-        if (r < m && colbase + c < m) s += fabs(Wl[(size_t)r * CW + c]);
-      fcol[r] = s;
+        if (r < m && colbase + c < m) sacc += fabs(Wl[(size_t)r * CW + c]);
+      fcol[r] = sacc;
     }
     cluster.sync();
     double mx = 0.0;
     for (int r = tid; r < m; r += GJC_NT) {
-      double s = 0.0;
-      for (int q = 0; q < CS; ++q) s += cluster.map_shared_rank(fcol, q)[r];
-      mx = fmax(mx, s);
+      double sacc = 0.0;
+      for (int q = 0; q < CS; ++q) sacc += cluster.map_shared_rank(fcol, q)[r];
+      mx = fmax(mx, sacc);
     }
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) redv[warp] = mx;
+    if (lane == 0) rk[warp] = mx;
     __syncthreads();
     mx = 0.0;
-    for (int w = 0; w < GJC_NT / 32; ++w) mx = fmax(mx, redv[w]);
+    for (int w = 0; w < GJC_NT / 32; ++w) mx = fmax(mx, rk[w]);
     tol = d.rcond * mx;
-    cluster.sync();  // fcol is reused below
+    cluster.sync();  // fcol / rk are reused below
   } else {
-    tol = d.tol[b];
+    tol = d.rcond * __longlong_as_double((long long)d.rsmax[b]);
     __syncthreads();
   }
-  (void)rs_part;
 
   int fail = -1;
   for (int kk = 0; kk < d.npiv; ++kk) {
     const int k = d.k0 + kk;
-    const int lk = k - d.c0;           // panel-local pivot column
-    const int owner = lk / CW;
+    const int lk = k - d.c0;  // panel-local pivot column
+    const int owner = lk / CW, lc = lk - owner * CW;
     double* myb = bc + (kk & 1) * (mp + 4);
-    if (rank == owner) {
-      const int lc = lk - owner * CW;
+    if (rank == owner && (mp > 256 || warp == 0)) {
+      // pivot search: first max |w_ik|, i >= k (one warp for short columns, the CTA above 256)
+      const int nth = mp > 256 ? GJC_NT : 32, me = mp > 256 ? tid : lane;
       double bv = -1.0;
       int bi = mp;
-      for (int i = k + tid; i < mp; i += GJC_NT) {
+      for (int i = k + me; i < mp; i += nth) {
         const double v = fabs(Wl[(size_t)i * CW + lc]);
         if (v > bv) { bv = v; bi = i; }
       }
@@ -141,17 +143,19 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
       }
-      if (lane == 0) { redv[warp] = bv; redi[warp] = bi; }
-      for (int i = tid; i < mp; i += GJC_NT) myb[i] = Wl[(size_t)i * CW + lc];
-      __syncthreads();
+      for (int i = me; i < mp; i += nth) myb[i] = Wl[(size_t)i * CW + lc];
+      if (mp > 256) {  // cross-warp: rk / okr are free between steps
+        int* redi = reinterpret_cast<int*>(okr);
+        if (lane == 0) { rk[warp] = bv; redi[warp] = bi; }
+        __syncthreads();
+        if (tid == 0)
+          for (int w = 1; w < GJC_NT / 32; ++w)
+            if (rk[w] > bv || (rk[w] == bv && redi[w] < bi)) { bv = rk[w]; bi = redi[w]; }
+      }
       if (tid == 0) {
-        double v = redv[0];
-        int i = redi[0];
-        for (int w = 1; w < GJC_NT / 32; ++w)
-          if (redv[w] > v || (redv[w] == v && redi[w] < i)) { v = redv[w]; i = redi[w]; }
-        myb[mp] = (double)i;
-        myb[mp + 1] = Wl[(size_t)i * CW + lc];
-        myb[mp + 2] = (k < m && v <= tol) ? 1.0 : 0.0;
+        myb[mp] = (double)bi;
+        myb[mp + 1] = Wl[(size_t)bi * CW + lc];
+        myb[mp + 2] = (k < m && bv <= tol) ? 1.0 : 0.0;
       }
     }
     cluster.sync();
@@ -159,110 +163,123 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
     const int p = (int)ob[mp];
     const double pv = ob[mp + 1];
     if (ob[mp + 2] != 0.0) { fail = k; break; }
-    // swapped multipliers f (row p gets old row k's value, row k the pivot's)
-    for (int i = tid; i < mp; i += GJC_NT) fcol[i] = ob[i];
-    __syncthreads();
-    if (tid == 0 && p != k) {
-      const double t = fcol[k];
-      fcol[k] = fcol[p];
-      fcol[p] = t;
-    }
     const double inv = 1.0 / pv;
+    // swapped multipliers (row p holds old row k's value, row k the pivot's), the
+    // new pivot row and the old row k
+    for (int i = tid; i < mp; i += GJC_NT) fcol[i] = ob[i == k ? p : (i == p ? k : i)];
     for (int c = tid; c < CW; c += GJC_NT) {
       okr[c] = Wl[(size_t)k * CW + c];
       rk[c] = Wl[(size_t)p * CW + c] * inv;
     }
+    if (tid == 0) piv_s[kk] = p;
     __syncthreads();
     for (int e = tid; e < mp * CW; e += GJC_NT) {
       const int i = e / CW, c = e - i * CW;
-      if (i == k) { Wl[e] = rk[c]; continue; }
-      const double src = i == p ? okr[c] : Wl[e];
-      Wl[e] = fma(-fcol[i], rk[c], src);
+      double v;
+      if (rank == owner && c == lc) v = i == k ? inv : -fcol[i] * inv;  // Gauss-Jordan column
+      else if (i == k) v = rk[c];
+      else v = fma(-fcol[i], rk[c], i == p ? okr[c] : Wl[e]);
+      Wl[e] = v;
     }
-    __syncthreads();
-    if (rank == owner) {  // in-place Gauss-Jordan column g
-      const int lc = lk - owner * CW;
-      for (int i = tid; i < mp; i += GJC_NT) Wl[(size_t)i * CW + lc] = i == k ? inv : -fcol[i] * inv;
-      if (!full && tid == 0) d.piv[(int64_t)b * (CS * CW) + kk] = p;
-    }
+    if (!full && rank == owner && tid == 0) d.piv[(int64_t)b * mp + k] = p;
     __syncthreads();
   }
 
-  if (fail >= 0) {
-    if (rank == 0 && tid == 0) {
-      const bool checked = !d.active_until || d.step < d.active_until[b];
-      if (checked) {
-        const int64_t slot = d.fail_map ? d.fail_map[b] : b;
-        if (d.fail_step[slot] < 0) {
-          d.fail_step[slot] = d.step;
-          d.fail_col[slot] = fail;
-        }
+  if (fail >= 0 && rank == 0 && tid == 0) {
+    const bool checked = !d.active_until || d.step < d.active_until[b];
+    if (checked) {
+      const int64_t slot = d.fail_map ? d.fail_map[b] : b;
+      if (d.fail_step[slot] < 0) {
+        d.fail_step[slot] = d.step;
+        d.fail_col[slot] = fail;
       }
-      if (!full) d.dead[b] = 1;
     }
+    if (!full) d.dead[b] = 1;
   }
   if (full) {
+    // column j of the result holds column dest(j) of D^{-1}: undo the swaps in reverse order
+    if (fail < 0 && tid == 0) {
+      for (int j = 0; j < mp; ++j) dest[j] = j;  // dest[pos] = original column now at pos
+      for (int kk = mp - 1; kk >= 0; --kk) {
+        const int p = piv_s[kk];
+        const int t = dest[kk];
+        dest[kk] = dest[p];
+        dest[p] = t;
+      }
+      for (int j = 0; j < mp; ++j) piv_s[dest[j]] = j;  // where each column goes
+    }
+    __syncthreads();
     double* O = d.out + ((d.idx_out ? d.idx_out[b] : (int64_t)b) + d.add_out) * (int64_t)mp * mp;
     for (int e = tid; e < mp * CW; e += GJC_NT) {
       const int r = e / CW, c = e - r * CW, gc = colbase + c;
-      if (gc >= mp) O[(int64_t)r * mp + gc - mp] = fail >= 0 ? 0.0 : Wl[e];
+      if (fail >= 0) O[(int64_t)r * mp + gc] = 0.0;
+      else O[(int64_t)r * mp + piv_s[gc]] = Wl[e];
     }
   } else if (fail < 0) {
     for (int e = tid; e < mp * CW; e += GJC_NT) {
       const int r = e / CW, c = e - r * CW;
-      Wg[(int64_t)r * W2 + colbase + c] = Wl[e];
+      Wg[(int64_t)r * LDW + colbase + c] = Wl[e];
     }
   }
   cluster.sync();  // no CTA leaves while others may still read its shared memory
 }
 
-// W = [D | I] per batch entry (panel mode) + singularity threshold; clears `dead`.
+// Panel mode set-up: W = D (zero padding columns), max row abs sum of the leading
+// m x m block (atomicMax on the bits: nonnegative doubles order like their bits).
+// rsmax and dead are zeroed by the caller.  One warp per (entry, row).
 __global__ void gjc_init_kernel(GjcDesc d) {
-  __shared__ double red[32];
-  const int mp = d.mp, W2 = 2 * mp;
-  for (int b = blockIdx.x; b < d.nbatch; b += gridDim.x) {
-    const double* A = d.in + ((d.idx_in ? d.idx_in[b] : (int64_t)b) + d.add_in) * (int64_t)mp * mp;
-    double* Wg = d.W + (int64_t)b * mp * W2;
-    double mx = 0.0;
-    for (int r = threadIdx.x >> 5; r < mp; r += blockDim.x >> 5) {
-      double s = 0.0;
-      for (int c = threadIdx.x & 31; c < W2; c += 32) {
-        const double v = c < mp ? A[(int64_t)r * mp + c] : (c - mp == r ? 1.0 : 0.0);
-        Wg[(int64_t)r * W2 + c] = v;
-        if (r < d.m && c < d.m) s += fabs(v);
-      }
-      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      mx = fmax(mx, s);
+  const int mp = d.mp, LDW = mp + 32, lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < (int64_t)d.nbatch * mp;
+       w += nw) {
+    const int b = (int)(w / mp), r = (int)(w - (int64_t)b * mp);
+    const double* A = d.in + ((d.idx_in ? d.idx_in[b] : (int64_t)b) + d.add_in) * (int64_t)mp * mp + (int64_t)r * mp;
+    double* Wr = d.W + ((int64_t)b * mp + r) * LDW;
+    double sacc = 0.0;
+    for (int c = lane; c < LDW; c += 32) {
+      const double v = c < mp ? A[c] : 0.0;
+      Wr[c] = v;
+      if (r < d.m && c < d.m) sacc += fabs(v);
     }
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double v = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
-      d.tol[b] = d.rcond * v;
-      d.dead[b] = 0;
-    }
-    __syncthreads();
+    for (int o = 16; o; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    if (lane == 0 && r < d.m) atomicMax(d.rsmax + b, (unsigned long long)__double_as_longlong(sacc));
   }
 }
 
-// D^{-1} = right half of W (zeros for failed entries).
+// Output column of every W column: the row swaps of all pivots, in reverse order,
+// applied to the columns (in-place Gauss-Jordan).  One thread per entry.
+__global__ void gjc_colmap_kernel(GjcDesc d) {
+  const int mp = d.mp;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < d.nbatch; b += gridDim.x * blockDim.x) {
+    int32_t* pos = d.colmap + (int64_t)b * mp;  // first: pos[j] = W column found at output position j
+    const int32_t* pv = d.piv + (int64_t)b * mp;
+    for (int j = 0; j < mp; ++j) pos[j] = j;
+    for (int k = mp - 1; k >= 0; --k) {
+      const int p = pv[k];
+      const int32_t t = pos[k];
+      pos[k] = pos[p];
+      pos[p] = t;
+    }
+  }
+}
+
+// D^{-1}[r][j] = W[r][colmap[j]] (zeros for failed entries).
 __global__ void gjc_extract_kernel(GjcDesc d) {
-  const int mp = d.mp, W2 = 2 * mp;
+  const int mp = d.mp, LDW = mp + 32;
   const int64_t per = (int64_t)mp * mp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)d.nbatch * per;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int b = (int)(e / per);
     const int64_t rc = e - (int64_t)b * per;
-    const int r = (int)(rc / mp), c = (int)(rc - (int64_t)r * mp);
+    const int r = (int)(rc / mp), j = (int)(rc - (int64_t)r * mp);
     double* O = d.out + ((d.idx_out ? d.idx_out[b] : (int64_t)b) + d.add_out) * per;
-    O[rc] = d.dead[b] ? 0.0 : d.W[(int64_t)b * mp * W2 + (int64_t)r * W2 + mp + c];
+    O[rc] = d.dead[b] ? 0.0 : d.W[((int64_t)b * mp + r) * LDW + d.colmap[(int64_t)b * mp + j]];
   }
 }
 
-// Trailing update after a panel (panel mode): for the columns [c0 + PW, 2 mp)
-//   X = Pi W_rest (the panel's row swaps, in order),  W_rest <- X + (T_K - E) X[K]
-// T_K = panel columns c0 .. c0+npiv-1 (written back by the panel kernel), E the unit
+// Update after a panel (panel mode), every W column outside the panel window
+// [c0, c0 + PW):  X = Pi W (the panel's row swaps, in order),  W <- X + (T_K - E) X[K]
+// T_K = the panel's pivot columns (written back by the panel kernel), E the unit
 // columns at the pivot rows K = k0 .. k0+npiv-1.  One CTA per (entry, 32-column
 // tile); the rank-npiv product runs on DMMA (m8n8k4): 8 warps, each a 16 x 16 tile
 // of a 64-row block.  mp <= GJC_MAXMP.
@@ -277,17 +294,17 @@ __global__ void __launch_bounds__(256) gjc_update_kernel(GjcDesc d, int ntiles) 
   __shared__ int npos;
   const int b = blockIdx.x / ntiles, tile = blockIdx.x - b * ntiles;
   if (b >= d.nbatch || d.dead[b]) return;
-  const int mp = d.mp, W2 = 2 * mp, npiv = d.npiv, k0 = d.k0;
-  const int cbeg = d.c0 + PW + tile * TN;
-  if (cbeg >= W2) return;
-  const int ncols = min(TN, W2 - cbeg);
-  double* Wg = d.W + (int64_t)b * mp * W2;
+  const int mp = d.mp, LDW = mp + 32, npiv = d.npiv, k0 = d.k0;
+  const int cbeg = tile * TN;
+  if (cbeg >= mp || (cbeg >= d.c0 && cbeg < d.c0 + PW)) return;  // the panel updated itself
+  const int ncols = min(TN, mp - cbeg);
+  double* Wg = d.W + (int64_t)b * mp * LDW;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int r = tid; r < mp; r += 256) rowmap[r] = -1;
   if (tid == 0) {  // net source row of every position the swaps touch
     int n = 0;
     for (int kk = 0; kk < npiv; ++kk) {
-      const int a = k0 + kk, p = d.piv[(int64_t)b * PW + kk];
+      const int a = k0 + kk, p = d.piv[(int64_t)b * mp + a];
       if (a == p) continue;
       int ia = -1, ip = -1;
       for (int j = 0; j < n; ++j) {
@@ -307,7 +324,7 @@ __global__ void __launch_bounds__(256) gjc_update_kernel(GjcDesc d, int ntiles) 
   for (int j = tid; j < n; j += 256) rowmap[pos[j]] = (int16_t)j;
   for (int e = tid; e < n * TN; e += 256) {
     const int j = e / TN, c = e - j * TN;
-    Xi[j][c] = c < ncols ? Wg[(int64_t)src[j] * W2 + cbeg + c] : 0.0;
+    Xi[j][c] = c < ncols ? Wg[(int64_t)src[j] * LDW + cbeg + c] : 0.0;
   }
   __syncthreads();
   for (int e = tid; e < PW * TN; e += 256) {
@@ -315,7 +332,7 @@ __global__ void __launch_bounds__(256) gjc_update_kernel(GjcDesc d, int ntiles) 
     double v = 0.0;
     if (kk < npiv && c < ncols) {
       const int r = k0 + kk, j = rowmap[r];
-      v = j >= 0 ? Xi[j][c] : Wg[(int64_t)r * W2 + cbeg + c];
+      v = j >= 0 ? Xi[j][c] : Wg[(int64_t)r * LDW + cbeg + c];
     }
     Xk[kk][c] = v;
   }
@@ -335,7 +352,7 @@ __global__ void __launch_bounds__(256) gjc_update_kernel(GjcDesc d, int ntiles) 
       for (int i = 0; i < 2; ++i) {
         const int r = r0 + wr + i * 8 + g, kk = k4 + t;
         double v = 0.0;
-        if (r < mp && kk < npiv) v = Wg[(int64_t)r * W2 + d.c0 + kk] - (r == k0 + kk ? 1.0 : 0.0);
+        if (r < mp && kk < npiv) v = Wg[(int64_t)r * LDW + d.c0 + kk] - (r == k0 + kk ? 1.0 : 0.0);
         a[i] = v;
       }
 #pragma unroll
@@ -357,7 +374,7 @@ __global__ void __launch_bounds__(256) gjc_update_kernel(GjcDesc d, int ntiles) 
         for (int h = 0; h < 2; ++h) {
           const int c = wc + j * 8 + 2 * t + h;
           if (c >= ncols) continue;
-          double* dst = Wg + (int64_t)r * W2 + cbeg + c;
+          double* dst = Wg + (int64_t)r * LDW + cbeg + c;
           const double x = jx >= 0 ? Xi[jx][c] : *dst;
           *dst = x + acc[i][j][h];
         }

@@ -23,6 +23,8 @@ ranks, split = bench.plan_params(name, 1)
 plan = btd.plan_build_arrays(torch.from_numpy(d).cuda(), torch.from_numpy(lo).cuda(), torch.from_numpy(up).cuda(),
                              ranks, split=split)
 del d, lo, up
+if len(sys.argv) > 3 and sys.argv[3] == "pinned":  # input in cudaHostAlloc memory instead of registered numpy
+    F = btd.pinned_array(F)
 lib = _native.load()
 for i in range(calls):
     t0 = time.perf_counter()
