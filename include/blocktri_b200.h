@@ -196,6 +196,7 @@ int btd_copy_columns(double* host, int64_t rows, int64_t K, int64_t c0, int64_t 
  *   btd_host_unpin  undoes btd_host_pin;
  *   btd_host_alloc / btd_host_free  page-locked allocations (solution arrays). */
 int btd_host_pin(void* ptr, int64_t nbytes, int* was_pinned);
+int btd_host_is_pinned(const void* ptr);  /* 1 when ptr lies in page-locked memory, else 0 */
 int btd_host_unpin(void* ptr);
 int btd_host_alloc(int64_t nbytes, void** out);
 int btd_host_free(void* ptr);

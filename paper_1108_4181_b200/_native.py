@@ -52,6 +52,7 @@ EXPORTS = (
     "btd_plan_phase_times",
     "btd_copy_columns",
     "btd_host_pin",
+    "btd_host_is_pinned",
     "btd_host_unpin",
     "btd_host_alloc",
     "btd_host_free",
@@ -132,6 +133,8 @@ def load():
     lib.btd_copy_columns.restype = i32
     lib.btd_host_pin.argtypes = [vp, i64, ctypes.POINTER(i32)]
     lib.btd_host_pin.restype = i32
+    lib.btd_host_is_pinned.argtypes = [vp]
+    lib.btd_host_is_pinned.restype = i32
     lib.btd_host_unpin.argtypes = [vp]
     lib.btd_host_unpin.restype = i32
     lib.btd_host_alloc.argtypes = [i64, ctypes.POINTER(vp)]

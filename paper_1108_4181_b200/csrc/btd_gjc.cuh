@@ -56,9 +56,11 @@ constexpr int GJC_NT = 256;
 
 template <int CW, int CS>
 struct GjcSmem {
+  static constexpr int LDS = CW + 1;  // odd row stride: column reads are bank-conflict free
   static size_t bytes(int mp) {
-    // W slice | fcol | 2 broadcast columns (+3 scalars each) | rk | ok | pivots + column map (ints)
-    return sizeof(double) * ((size_t)mp * CW + mp + 2 * ((size_t)mp + 4) + 2 * CW) + sizeof(int) * 2 * (size_t)mp;
+    // W slice | fcol | 2 broadcast columns (+3 scalars each) | rk | ok | reduction | pivots + column map
+    return sizeof(double) * ((size_t)mp * LDS + mp + 2 * ((size_t)mp + 4) + 2 * CW + 2 * (GJC_NT / 32)) +
+           sizeof(int) * 2 * (size_t)mp;
   }
 };
 
@@ -66,19 +68,24 @@ struct GjcSmem {
 // pivot the slice holds D^{-1} with its columns permuted by the row swaps, which
 // the store undoes (the swaps, in reverse order, applied to the columns).
 // Panel mode: the pivot columns end up as T_K (see the file comment).
+// Per pivot the owning CTA PUSHES the pivot column and (p, pivot, fail) into every
+// CTA's shared memory (DSMEM stores), so after the cluster barrier all reads are local.
 template <int CW, int CS>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_kernel(GjcDesc d) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
+  constexpr int LDS = GjcSmem<CW, CS>::LDS;
   extern __shared__ __align__(16) double sm[];
   const int mp = d.mp, m = d.m, LDW = mp + 32;
-  double* Wl = sm;                          // [mp][CW]
-  double* fcol = Wl + (size_t)mp * CW;      // [mp]  swapped multipliers of this step
-  double* bc = fcol + mp;                   // [2][mp + 4]: column, p, pv, fail
+  double* Wl = sm;                          // [mp][LDS]
+  double* fcol = Wl + (size_t)mp * LDS;     // [mp]  swapped multipliers of this step
+  double* bc = fcol + mp;                   // [2][mp + 4]: column, p, pv, fail (written by the owner)
   double* rk = bc + 2 * (mp + 4);           // [CW]  new pivot row
   double* okr = rk + CW;                    // [CW]  old row k (moves to row p)
-  int* piv_s = reinterpret_cast<int*>(okr + CW);  // [mp] pivot row of every step (full mode)
-  int* dest = piv_s + mp;                   // [mp] output column of every global column
+  double* redv = okr + CW;                  // [NT/32] cross-warp pivot search
+  int* redi = reinterpret_cast<int*>(redv + GJC_NT / 32);
+  int* piv_s = redi + 2 * (GJC_NT / 32);    // [mp] pivot row of every step (full mode)
+  int* dest = piv_s + mp;                   // [mp]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rank = (int)cluster.block_rank();
   const int b = blockIdx.x / CS;
@@ -91,7 +98,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
 
   for (int e = tid; e < mp * CW; e += GJC_NT) {
     const int r = e / CW, c = e - r * CW, gc = colbase + c;
-    Wl[e] = full ? A[(int64_t)r * mp + gc] : Wg[(int64_t)r * LDW + gc];
+    Wl[r * LDS + c] = full ? A[(int64_t)r * mp + gc] : Wg[(int64_t)r * LDW + gc];
   }
   double tol;
   if (full) {
@@ -101,7 +108,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
     for (int r = tid; r < mp; r += GJC_NT) {
       double sacc = 0.0;
       for (int c = 0; c < CW; ++c)
-        if (r < m && colbase + c < m) sacc += fabs(Wl[(size_t)r * CW + c]);
+        if (r < m && colbase + c < m) sacc += fabs(Wl[r * LDS + c]);
       fcol[r] = sacc;
     }
     cluster.sync();
@@ -112,12 +119,12 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
       mx = fmax(mx, sacc);
     }
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) rk[warp] = mx;
+    if (lane == 0) redv[warp] = mx;
     __syncthreads();
     mx = 0.0;
-    for (int w = 0; w < GJC_NT / 32; ++w) mx = fmax(mx, rk[w]);
+    for (int w = 0; w < GJC_NT / 32; ++w) mx = fmax(mx, redv[w]);
     tol = d.rcond * mx;
-    cluster.sync();  // fcol / rk are reused below
+    cluster.sync();  // fcol / redv are reused below
   } else {
     tol = d.rcond * __longlong_as_double((long long)d.rsmax[b]);
     __syncthreads();
@@ -128,14 +135,15 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
     const int k = d.k0 + kk;
     const int lk = k - d.c0;  // panel-local pivot column
     const int owner = lk / CW, lc = lk - owner * CW;
-    double* myb = bc + (kk & 1) * (mp + 4);
-    if (rank == owner && (mp > 256 || warp == 0)) {
-      // pivot search: first max |w_ik|, i >= k (one warp for short columns, the CTA above 256)
-      const int nth = mp > 256 ? GJC_NT : 32, me = mp > 256 ? tid : lane;
+    const int boff = (kk & 1) * (mp + 4);
+    if (rank == owner) {
+      // pivot: first max |w_ik|, i >= k.  Short columns: every warp scans all rows (no
+      // barrier); long ones: the warps split the rows and meet in shared memory.
+      const bool split = mp > 256;
       double bv = -1.0;
       int bi = mp;
-      for (int i = k + me; i < mp; i += nth) {
-        const double v = fabs(Wl[(size_t)i * CW + lc]);
+      for (int i = k + (split ? tid : lane); i < mp; i += (split ? GJC_NT : 32)) {
+        const double v = fabs(Wl[i * LDS + lc]);
         if (v > bv) { bv = v; bi = i; }
       }
       for (int o = 16; o; o >>= 1) {
@@ -143,23 +151,28 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
       }
-      for (int i = me; i < mp; i += nth) myb[i] = Wl[(size_t)i * CW + lc];
-      if (mp > 256) {  // cross-warp: rk / okr are free between steps
-        int* redi = reinterpret_cast<int*>(okr);
-        if (lane == 0) { rk[warp] = bv; redi[warp] = bi; }
+      if (split) {
+        if (lane == 0) { redv[warp] = bv; redi[warp] = bi; }
         __syncthreads();
-        if (tid == 0)
-          for (int w = 1; w < GJC_NT / 32; ++w)
-            if (rk[w] > bv || (rk[w] == bv && redi[w] < bi)) { bv = rk[w]; bi = redi[w]; }
+        bv = redv[0];
+        bi = redi[0];
+        for (int w = 1; w < GJC_NT / 32; ++w)
+          if (redv[w] > bv || (redv[w] == bv && redi[w] < bi)) { bv = redv[w]; bi = redi[w]; }
       }
-      if (tid == 0) {
-        myb[mp] = (double)bi;
-        myb[mp + 1] = Wl[(size_t)bi * CW + lc];
-        myb[mp + 2] = (k < m && bv <= tol) ? 1.0 : 0.0;
+      // push the (pre-swap) column and the pivot into every CTA of the cluster
+      for (int e = tid; e < CS * mp; e += GJC_NT) {
+        const int q = e / mp, i = e - q * mp;
+        cluster.map_shared_rank(bc, q)[boff + i] = Wl[i * LDS + lc];
+      }
+      if (tid < CS) {
+        double* rb = cluster.map_shared_rank(bc, tid) + boff;
+        rb[mp] = (double)bi;
+        rb[mp + 1] = Wl[bi * LDS + lc];
+        rb[mp + 2] = (k < m && bv <= tol) ? 1.0 : 0.0;
       }
     }
     cluster.sync();
-    const double* ob = cluster.map_shared_rank(myb, owner);
+    const double* ob = bc + boff;
     const int p = (int)ob[mp];
     const double pv = ob[mp + 1];
     if (ob[mp + 2] != 0.0) { fail = k; break; }
@@ -168,8 +181,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
     // new pivot row and the old row k
     for (int i = tid; i < mp; i += GJC_NT) fcol[i] = ob[i == k ? p : (i == p ? k : i)];
     for (int c = tid; c < CW; c += GJC_NT) {
-      okr[c] = Wl[(size_t)k * CW + c];
-      rk[c] = Wl[(size_t)p * CW + c] * inv;
+      okr[c] = Wl[k * LDS + c];
+      rk[c] = Wl[p * LDS + c] * inv;
     }
     if (tid == 0) piv_s[kk] = p;
     __syncthreads();
@@ -178,8 +191,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
       double v;
       if (rank == owner && c == lc) v = i == k ? inv : -fcol[i] * inv;  // Gauss-Jordan column
       else if (i == k) v = rk[c];
-      else v = fma(-fcol[i], rk[c], i == p ? okr[c] : Wl[e]);
-      Wl[e] = v;
+      else v = fma(-fcol[i], rk[c], i == p ? okr[c] : Wl[i * LDS + c]);
+      Wl[i * LDS + c] = v;
     }
     if (!full && rank == owner && tid == 0) d.piv[(int64_t)b * mp + k] = p;
     __syncthreads();
@@ -213,15 +226,15 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
     for (int e = tid; e < mp * CW; e += GJC_NT) {
       const int r = e / CW, c = e - r * CW, gc = colbase + c;
       if (fail >= 0) O[(int64_t)r * mp + gc] = 0.0;
-      else O[(int64_t)r * mp + piv_s[gc]] = Wl[e];
+      else O[(int64_t)r * mp + piv_s[gc]] = Wl[r * LDS + c];
     }
   } else if (fail < 0) {
     for (int e = tid; e < mp * CW; e += GJC_NT) {
       const int r = e / CW, c = e - r * CW;
-      Wg[(int64_t)r * LDW + colbase + c] = Wl[e];
+      Wg[(int64_t)r * LDW + colbase + c] = Wl[r * LDS + c];
     }
   }
-  cluster.sync();  // no CTA leaves while others may still read its shared memory
+  cluster.sync();  // no CTA leaves while others may still write into its shared memory
 }
 
 // Panel mode set-up: W = D (zero padding columns), max row abs sum of the leading

@@ -291,6 +291,8 @@ def _pin_input(a):
     Returns True when the buffer is page-locked."""
     import weakref
 
+    if _native.load().btd_host_is_pinned(ctypes.c_void_p(a.ctypes.data)):
+        return True  # already page-locked: pinned_array / pinned_empty, a pinned torch tensor's view
     owner = a
     while isinstance(owner.base, np.ndarray):
         owner = owner.base
