@@ -653,25 +653,15 @@ void launch_inv(btd_plan& pl, int nbatch, const double* in, const int64_t* idx_i
 template <int MP, int KT, int WR, int WC, int NF = -1, int NY = -1, int PF = -1, int MINB = 1, int FULL = 0>
 void launch_chain_t(const ChainArgs& a, bool fwd, cudaStream_t st) {
   using Cfg = ChainCfg<MP, KT, WR, WC, NF, NY, PF>;
-  // BTD_CHAIN_DBUF=1: double-buffered chain state (one barrier per row) where it fits in smem
-  static int dbuf = -1;
-  if (dbuf < 0) dbuf = getenv("BTD_CHAIN_DBUF") ? atoi(getenv("BTD_CHAIN_DBUF")) : 0;
-  const size_t tile = (size_t)MP * Cfg::LD * sizeof(double);
-  const size_t base = (size_t)(fwd ? Cfg::FWD_BUFS : Cfg::BWD_BUFS) * tile;
-  const bool db = dbuf && base + tile <= 227 * 1024;
-  const size_t smem = base + (db ? tile : 0);
+  const size_t smem = (size_t)(fwd ? Cfg::FWD_BUFS : Cfg::BWD_BUFS) * MP * Cfg::LD * sizeof(double);
   const int64_t ntile = (a.K + KT - 1) / KT;
   dim3 grid((unsigned)ntile, (unsigned)a.nr);
   if (fwd) {
-    auto k = db ? chain_fwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB, FULL, 1>
-                : chain_fwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB, FULL, 0>;
-    set_smem_attr((const void*)k, smem);
-    k<<<grid, Cfg::NT, smem, st>>>(a);
+    set_smem_attr((const void*)chain_fwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB, FULL>, smem);
+    chain_fwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB, FULL><<<grid, Cfg::NT, smem, st>>>(a);
   } else {
-    auto k = db ? chain_bwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB, FULL, 1>
-                : chain_bwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB, FULL, 0>;
-    set_smem_attr((const void*)k, smem);
-    k<<<grid, Cfg::NT, smem, st>>>(a);
+    set_smem_attr((const void*)chain_bwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB, FULL>, smem);
+    chain_bwd_kernel<MP, KT, WR, WC, NF, NY, PF, MINB, FULL><<<grid, Cfg::NT, smem, st>>>(a);
   }
   CK_LAUNCH();
 }

@@ -326,11 +326,7 @@ BTD_DEVINL void group_load(double2 (&buf)[PF][TM], const double* __restrict__ p,
 // Forward sweep.  Per interior row j, three segments stream through the same
 // register ring:  seg0 acc += AD_j y_{j-1};  seg1 ser += Tb_{j-1} y_{j-1};
 // seg2 acc += Dinv_j f_g.  (At j = 0, y_{-1} = 0 and seg1 reuses Tb_0.)
-// DB_: double-buffered chain state -- row j reads y_{j-1} from one tile and writes y_j
-// into the other, so a row needs ONE barrier (its end: y_j complete, next F tile
-// landed) instead of two (the write-after-read barrier before overwriting y_{j-1}).
-template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1, int MINB_ = 1, int FULL_ = 0,
-          int DB_ = 0>
+template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1, int MINB_ = 1, int FULL_ = 0>
 __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_fwd_kernel(ChainArgs a) {
   using Cfg = ChainCfg<MP, KT, WR, WC, NF_, NY_, PF_>;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, LD = Cfg::LD, NT = Cfg::NT, PF = Cfg::PF, GPS = Cfg::GPS;
@@ -338,7 +334,6 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_fwd_kernel(ChainArg
   extern __shared__ __align__(16) double sm[];
   double* Ys = sm;
   double* Fs = sm + MP * LD;  // ring of NF F tiles
-  double* Ys1 = sm + (1 + NF) * MP * LD;  // second state tile (DB_)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wr = warp / WC, wc = warp % WC;
@@ -347,7 +342,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_fwd_kernel(ChainArg
   const int64_t c0 = (int64_t)blockIdx.x * KT;
   const int64_t K = a.K;
   const bool vec = (K % 2) == 0;
-  for (int e = tid; e < (Cfg::FWD_BUFS + DB_) * MP * LD; e += NT) sm[e] = 0.0;
+  for (int e = tid; e < Cfg::FWD_BUFS * MP * LD; e += NT) sm[e] = 0.0;
   __syncthreads();
 
   const int64_t lo = a.lo[q];
@@ -390,8 +385,6 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_fwd_kernel(ChainArg
   for (int j = 0; j < nint; ++j) {
     const int64_t gr = lo + 1 + j;
     const double* Fcur = Fs + (j % NF) * MP * LD;
-    const double* Ycur = (DB_ && (j & 1)) ? Ys1 : Ys;  // y_{j-1}
-    double* Ynext = DB_ ? ((j & 1) ? Ys : Ys1) : Ys;  // y_j
     if constexpr (Cfg::PREF) {  // L2 prefetch: row j+PD's factor blocks (this warp's rows), F tile
       const int jp = j + Cfg::PD;
       if (jp < nint) {
@@ -429,23 +422,22 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_fwd_kernel(ChainArg
         if (frows > 0)
           nx = frow + (fseg == 0 ? 0 : (fseg == 1 ? tb_off - (frow0 ? 0 : blk) : dinv_off)) + fgrp * 8 * PF;
         if (seg == 0)
-          group_mma<MP, TM, TN, PF>(acc, buf, nx, Ycur + cw0, LD, grp * PF, g, t);
+          group_mma<MP, TM, TN, PF>(acc, buf, nx, Ys + cw0, LD, grp * PF, g, t);
         else if (seg == 1)
-          group_mma<MP, TM, TN, PF>(ser, buf, nx, Ycur + cw0, LD, grp * PF, g, t);
+          group_mma<MP, TM, TN, PF>(ser, buf, nx, Ys + cw0, LD, grp * PF, g, t);
         else
           group_mma<MP, TM, TN, PF>(acc, buf, nx, Fcur + cw0, LD, grp * PF, g, t);
       }
     }
-    if constexpr (!DB_) group_sync<WR, WC>(wc);  // every warp is done reading y_{j-1}
-    store_smem(acc, Ynext, LD, r0, cw0, g, t);
+    group_sync<WR, WC>(wc);
+    store_smem(acc, Ys, LD, r0, cw0, g, t);
     store_tile<TM, TN, FULL_ != 0>(acc, a.X + gr * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
     zero_acc(acc);
     cp_async_wait<NF - 2>();  // row j+1's F tile has landed
     group_sync<WR, WC>(wc);
   }
   cp_async_wait<0>();
-  const double* Ylast = (DB_ && (nint & 1)) ? Ys1 : Ys;  // y_{nint-1}
-  wgemm<MP, TM, TN, 2>(ser, a.Tb + (slot0 + nint - 1) * blk + r0 * MP, Ylast + cw0, LD, g, t);
+  wgemm<MP, TM, TN, 2>(ser, a.Tb + (slot0 + nint - 1) * blk + r0 * MP, Ys + cw0, LD, g, t);
   store_tile(ser, a.base + (int64_t)q * a.base_stride, K, r0, c0 + cw0, MP, g, t, vec);
 }
 
@@ -464,8 +456,7 @@ BTD_DEVINL void load_smem(double (&acc)[TM][TN][2], const double* Ys, int ld, in
 
 // Backward sweep: per row j (descending) two segments through one ring:
 // seg0 acc += G_j x~_q ; seg1 acc += S_j x_{j+1}, with acc initialised to y_j.
-template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1, int MINB_ = 1, int FULL_ = 0,
-          int DB_ = 0>
+template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1, int MINB_ = 1, int FULL_ = 0>
 __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_bwd_kernel(ChainArgs a) {
   using Cfg = ChainCfg<MP, KT, WR, WC, NF_, NY_, PF_>;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, LD = Cfg::LD, NT = Cfg::NT, PF = Cfg::PF, GPS = Cfg::GPS;
@@ -474,7 +465,6 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_bwd_kernel(ChainArg
   double* Xq = sm;
   double* Xn = sm + MP * LD;
   double* Ysr = sm + 2 * MP * LD;  // ring of NY y tiles (NY > 0)
-  double* Xn1 = sm + (2 + NY) * MP * LD;  // second state tile (DB_, see chain_fwd_kernel)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wr = warp / WC, wc = warp % WC;
@@ -483,7 +473,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_bwd_kernel(ChainArg
   const int64_t c0 = (int64_t)blockIdx.x * KT;
   const int64_t K = a.K;
   const bool vec = (K % 2) == 0;
-  for (int e = tid; e < (Cfg::BWD_BUFS + DB_) * MP * LD; e += NT) sm[e] = 0.0;
+  for (int e = tid; e < Cfg::BWD_BUFS * MP * LD; e += NT) sm[e] = 0.0;
   __syncthreads();
 
   const int64_t lo = a.lo[q];
@@ -528,8 +518,6 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_bwd_kernel(ChainArg
   for (int jj = 0; jj < nint; ++jj) {
     const int j = nint - 1 - jj;
     const int64_t gr = lo + 1 + j;
-    const double* Xcur = (DB_ && (jj & 1)) ? Xn1 : Xn;  // x_{j+1}
-    double* Xnext = DB_ ? ((jj & 1) ? Xn : Xn1) : Xn;   // x_j
     if constexpr (Cfg::PREF) {  // L2 prefetch: row j-PD's G and S blocks (this warp's rows), y tile
       const int jp = j - Cfg::PD;
       if (jp >= 0) {
@@ -570,11 +558,11 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_bwd_kernel(ChainArg
           }
         }
         const double* nx = frows > 0 ? frow + (fseg ? s_off : 0) + fgrp * 8 * PF : nullptr;
-        group_mma<MP, TM, TN, PF>(acc, buf, nx, (seg == 0 ? Xq : Xcur) + cw0, LD, grp * PF, g, t);
+        group_mma<MP, TM, TN, PF>(acc, buf, nx, (seg == 0 ? Xq : Xn) + cw0, LD, grp * PF, g, t);
       }
     }
-    if constexpr (!DB_) group_sync<WR, WC>(wc);  // every warp is done reading x_{j+1}
-    store_smem(acc, Xnext, LD, r0, cw0, g, t);
+    group_sync<WR, WC>(wc);
+    store_smem(acc, Xn, LD, r0, cw0, g, t);
     store_tile<TM, TN, FULL_ != 0>(acc, a.X + gr * rowK, K, r0, c0 + cw0, a.m, g, t, vec);
     if constexpr (NY > 1) cp_async_wait<NY - 2>();
     group_sync<WR, WC>(wc);
