@@ -577,8 +577,9 @@ void launch_inv(btd_plan& pl, int nbatch, const double* in, const int64_t* idx_i
     if (ws.bytes < (size_t)chunk * wbytes) ws.alloc((size_t)chunk * wbytes);
     const size_t aux = (size_t)chunk * (2 * (size_t)mp * sizeof(int32_t) + sizeof(unsigned long long) + sizeof(int32_t));
     if (pl.gjc_aux.bytes < aux) pl.gjc_aux.alloc(aux);
-    const size_t smem = GjcSmem<8, 4>::bytes(mp);
-    set_smem_attr((const void*)gjc_panel_kernel<8, 4>, smem);
+    // long panels: 1024 threads per CTA (one CTA per SM anyway: the slice is ~150 KB)
+    const size_t smem = GjcSmem<8, 4, 1024>::bytes(mp);
+    set_smem_attr((const void*)gjc_panel_kernel<8, 4, 1024>, smem);
     for (int b0 = 0; b0 < nbatch; b0 += chunk) {
       GjcDesc c = g;
       c.nbatch = std::min(chunk, nbatch - b0);
@@ -604,7 +605,7 @@ void launch_inv(btd_plan& pl, int nbatch, const double* in, const int64_t* idx_i
       const int ntiles = (mp + 31) / 32;
       for (int k0 = 0; k0 < mp; k0 += PW) {
         c.c0 = k0; c.k0 = k0; c.npiv = std::min(PW, mp - k0);
-        gjc_panel_kernel<8, 4><<<c.nbatch * 4, GJC_NT, smem, st>>>(c);
+        gjc_panel_kernel<8, 4, 1024><<<c.nbatch * 4, 1024, smem, st>>>(c);
         CK_LAUNCH();
         gjc_update_kernel<PW><<<c.nbatch * ntiles, 256, 0, st>>>(c, ntiles);
         CK_LAUNCH();

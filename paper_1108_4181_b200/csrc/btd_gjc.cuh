@@ -54,12 +54,12 @@ struct GjcDesc {
 
 constexpr int GJC_NT = 256;
 
-template <int CW, int CS>
+template <int CW, int CS, int NT = GJC_NT>
 struct GjcSmem {
   static constexpr int LDS = CW + 1;  // odd row stride: column reads are bank-conflict free
   static size_t bytes(int mp) {
     // W slice | fcol | 2 broadcast columns (+3 scalars each) | rk | ok | reduction | pivots + column map
-    return sizeof(double) * ((size_t)mp * LDS + mp + 2 * ((size_t)mp + 4) + 2 * CW + 2 * (GJC_NT / 32)) +
+    return sizeof(double) * ((size_t)mp * LDS + mp + 2 * ((size_t)mp + 4) + 2 * CW + 2 * (NT / 32)) +
            sizeof(int) * 2 * (size_t)mp;
   }
 };
@@ -70,11 +70,11 @@ struct GjcSmem {
 // Panel mode: the pivot columns end up as T_K (see the file comment).
 // Per pivot the owning CTA PUSHES the pivot column and (p, pivot, fail) into every
 // CTA's shared memory (DSMEM stores), so after the cluster barrier all reads are local.
-template <int CW, int CS>
-__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_kernel(GjcDesc d) {
+template <int CW, int CS, int NT = GJC_NT>
+__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(NT) gjc_panel_kernel(GjcDesc d) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
-  constexpr int LDS = GjcSmem<CW, CS>::LDS;
+  constexpr int LDS = GjcSmem<CW, CS, NT>::LDS;
   extern __shared__ __align__(16) double sm[];
   const int mp = d.mp, m = d.m, LDW = mp + 32;
   double* Wl = sm;                          // [mp][LDS]
@@ -83,8 +83,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
   double* rk = bc + 2 * (mp + 4);           // [CW]  new pivot row
   double* okr = rk + CW;                    // [CW]  old row k (moves to row p)
   double* redv = okr + CW;                  // [NT/32] cross-warp pivot search
-  int* redi = reinterpret_cast<int*>(redv + GJC_NT / 32);
-  int* piv_s = redi + 2 * (GJC_NT / 32);    // [mp] pivot row of every step (full mode)
+  int* redi = reinterpret_cast<int*>(redv + NT / 32);
+  int* piv_s = redi + 2 * (NT / 32);    // [mp] pivot row of every step (full mode)
   int* dest = piv_s + mp;                   // [mp]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rank = (int)cluster.block_rank();
@@ -96,7 +96,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
   const double* A = full ? d.in + ((d.idx_in ? d.idx_in[b] : (int64_t)b) + d.add_in) * (int64_t)mp * mp : nullptr;
   double* Wg = full ? nullptr : d.W + (int64_t)b * mp * LDW;
 
-  for (int e = tid; e < mp * CW; e += GJC_NT) {
+  for (int e = tid; e < mp * CW; e += NT) {
     const int r = e / CW, c = e - r * CW, gc = colbase + c;
     Wl[r * LDS + c] = full ? A[(int64_t)r * mp + gc] : Wg[(int64_t)r * LDW + gc];
   }
@@ -105,7 +105,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
     // singularity threshold: max row abs sum of the leading m x m block; each CTA
     // sums its columns, the partials meet through DSMEM
     __syncthreads();
-    for (int r = tid; r < mp; r += GJC_NT) {
+    for (int r = tid; r < mp; r += NT) {
       double sacc = 0.0;
       for (int c = 0; c < CW; ++c)
         if (r < m && colbase + c < m) sacc += fabs(Wl[r * LDS + c]);
@@ -113,7 +113,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
     }
     cluster.sync();
     double mx = 0.0;
-    for (int r = tid; r < m; r += GJC_NT) {
+    for (int r = tid; r < m; r += NT) {
       double sacc = 0.0;
       for (int q = 0; q < CS; ++q) sacc += cluster.map_shared_rank(fcol, q)[r];
       mx = fmax(mx, sacc);
@@ -122,7 +122,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
     if (lane == 0) redv[warp] = mx;
     __syncthreads();
     mx = 0.0;
-    for (int w = 0; w < GJC_NT / 32; ++w) mx = fmax(mx, redv[w]);
+    for (int w = 0; w < NT / 32; ++w) mx = fmax(mx, redv[w]);
     tol = d.rcond * mx;
     cluster.sync();  // fcol / redv are reused below
   } else {
@@ -142,7 +142,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
       const bool split = mp > 256;
       double bv = -1.0;
       int bi = mp;
-      for (int i = k + (split ? tid : lane); i < mp; i += (split ? GJC_NT : 32)) {
+      for (int i = k + (split ? tid : lane); i < mp; i += (split ? NT : 32)) {
         const double v = fabs(Wl[i * LDS + lc]);
         if (v > bv) { bv = v; bi = i; }
       }
@@ -156,11 +156,11 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
         __syncthreads();
         bv = redv[0];
         bi = redi[0];
-        for (int w = 1; w < GJC_NT / 32; ++w)
+        for (int w = 1; w < NT / 32; ++w)
           if (redv[w] > bv || (redv[w] == bv && redi[w] < bi)) { bv = redv[w]; bi = redi[w]; }
       }
       // push the (pre-swap) column and the pivot into every CTA of the cluster
-      for (int e = tid; e < CS * mp; e += GJC_NT) {
+      for (int e = tid; e < CS * mp; e += NT) {
         const int q = e / mp, i = e - q * mp;
         cluster.map_shared_rank(bc, q)[boff + i] = Wl[i * LDS + lc];
       }
@@ -179,14 +179,14 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
     const double inv = 1.0 / pv;
     // swapped multipliers (row p holds old row k's value, row k the pivot's), the
     // new pivot row and the old row k
-    for (int i = tid; i < mp; i += GJC_NT) fcol[i] = ob[i == k ? p : (i == p ? k : i)];
-    for (int c = tid; c < CW; c += GJC_NT) {
+    for (int i = tid; i < mp; i += NT) fcol[i] = ob[i == k ? p : (i == p ? k : i)];
+    for (int c = tid; c < CW; c += NT) {
       okr[c] = Wl[k * LDS + c];
       rk[c] = Wl[p * LDS + c] * inv;
     }
     if (tid == 0) piv_s[kk] = p;
     __syncthreads();
-    for (int e = tid; e < mp * CW; e += GJC_NT) {
+    for (int e = tid; e < mp * CW; e += NT) {
       const int i = e / CW, c = e - i * CW;
       double v;
       if (rank == owner && c == lc) v = i == k ? inv : -fcol[i] * inv;  // Gauss-Jordan column
@@ -223,13 +223,13 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(GJC_NT) gjc_panel_k
     }
     __syncthreads();
     double* O = d.out + ((d.idx_out ? d.idx_out[b] : (int64_t)b) + d.add_out) * (int64_t)mp * mp;
-    for (int e = tid; e < mp * CW; e += GJC_NT) {
+    for (int e = tid; e < mp * CW; e += NT) {
       const int r = e / CW, c = e - r * CW, gc = colbase + c;
       if (fail >= 0) O[(int64_t)r * mp + gc] = 0.0;
       else O[(int64_t)r * mp + piv_s[gc]] = Wl[r * LDS + c];
     }
   } else if (fail < 0) {
-    for (int e = tid; e < mp * CW; e += GJC_NT) {
+    for (int e = tid; e < mp * CW; e += NT) {
       const int r = e / CW, c = e - r * CW;
       Wg[(int64_t)r * LDW + colbase + c] = Wl[r * LDS + c];
     }
