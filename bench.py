@@ -464,6 +464,9 @@ def run_b200(args):
     if sharded:
         import torch.distributed as dist
 
+        if backend == "nccl":  # communicator set-up on stderr: ranks, channels, NVLS / CollNet use
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV")
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
         dist.init_process_group(backend, rank=rank, world_size=world,
@@ -481,9 +484,14 @@ def run_b200(args):
 
     # every rank draws the same global matrix / RHS (seeded numpy stream) and keeps its rows
     t0 = time.perf_counter()
-    host = make_inputs(name)
+    if args.inputs == "numpy":
+        host = make_inputs(name)
+        diag, lower, upper = (torch.from_numpy(a).cuda() for a in host[:3])
+    else:  # --inputs device (A/B only): torch Philox on the device, no parity report
+        diag, lower, upper, Fdev = configs.generate(name, device="cuda")
+        host = (None, None, None, Fdev.cpu().numpy())
+        del Fdev
     gen_s = time.perf_counter() - t0
-    diag, lower, upper = (torch.from_numpy(a).cuda() for a in host[:3])
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     if not sharded:
@@ -499,6 +507,9 @@ def run_b200(args):
         handle = plan.h
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
+    if args.inputs == "numpy":  # the residual re-uploads the matrix from the host arrays
+        del diag, lower, upper
+        torch.cuda.empty_cache()
     Fh = np.ascontiguousarray(host[3][row_lo:row_hi])
     F = torch.from_numpy(Fh).cuda()
     X = torch.empty_like(F)
@@ -563,12 +574,15 @@ def run_b200(args):
 
     res = None
     if not args.no_check:
+        if args.inputs == "numpy":
+            diag, lower, upper = (torch.from_numpy(a).cuda() for a in host[:3])
         res = (residual_check_sharded(torch, dist, X, F, diag, lower, upper, row_lo, row_hi) if sharded
                else residual_check(torch, X, F, diag, lower, upper))
-    del diag, lower, upper
+    if args.inputs != "numpy" or not args.no_check:
+        del diag, lower, upper
     torch.cuda.empty_cache()
     par = None
-    if not args.no_check and rank == 0:
+    if not args.no_check and rank == 0 and args.inputs == "numpy":
         try:
             par = parity_report(name, X, host, (row_lo, row_hi), ranks)
         except Exception as exc:  # the report must not kill the bench line
@@ -679,6 +693,11 @@ def run_b200(args):
                            "frac": t_roof * 1e3 / ms_step, "fp64_tflops_peak": fp64, "hbm_gbs_peak": hbm},
         "phases_ms": {"forward": ph[0], "interface_tree": ph[1], "backward": ph[2], "total": ph[3]},
         "per_rank": per_rank,
+        "collectives": ({"backend": backend, "world": world,
+                         "nccl_version": ".".join(str(v) for v in torch.cuda.nccl.version())
+                         if backend == "nccl" else None,
+                         "per_solve": "all-gather of one carry block per rank + all-gather of the crossing "
+                                      "tree-node partial sums (summed in rank order)"} if sharded else None),
         "plan_build_s": build_s,
         "input_generation_s": gen_s,
         "rel_residual": res,
@@ -806,6 +825,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use the row-sharded NCCL path even on one GPU")
+    ap.add_argument("--inputs", default="numpy", choices=["numpy", "device"],
+                    help="numpy: the seeded numpy stream (reference-golden inputs, parity report); "
+                         "device: torch Philox on the GPU (A/B runs only)")
     args = ap.parse_args()
     _stdout_to_stderr()
     if args.impl == "reference":

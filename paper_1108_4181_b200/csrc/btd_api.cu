@@ -714,6 +714,9 @@ bool launch_stream(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
 
 // Chain-kernel configuration per padded block order (MP, KT, warp rows x warp cols).
 // BTD_CHAIN_VARIANT selects alternatives for tuning experiments.
+// True when a KT-column tiling of this batch fills less than one wave of 148 SMs.
+bool under_wave(const ChainArgs& a, int kt) { return (int64_t)a.nr * ((a.K + kt - 1) / kt) < 148; }
+
 void launch_chain_slice(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st);
 
 // Sweep kernels index ranges by blockIdx.y (at most 65535): more ranges (ranks * split up to
@@ -769,7 +772,11 @@ void launch_chain_slice(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t s
       else if (variant == 20) launch_chain_t<64, 128, 8, 2, 2, 0, 8>(a, fwd, st);
       // measured best (c2, profiles/r01_chain_ab.txt): 128-column tiles of 2 x 8 warps with
       // per-column-group barriers in both directions (bwd 9.96 -> 9.54 ms vs 32-column tiles);
-      // forward factor fragments 8 pair steps ahead (13.76 -> 13.66 ms)
+      // forward factor fragments 8 pair steps ahead (13.76 -> 13.66 ms).  Narrow batches
+      // (host-pipeline chunks, small K) whose 128-column grid would leave SMs idle take
+      // 32-column tiles: the sweep is a chain of L row steps, so its latency falls with
+      // the work per CTA.
+      else if (under_wave(a, 128)) launch_chain_auto<64, 32, 8, 1>(a, fwd, st);
       else if (fwd) launch_chain_auto<64, 128, 8, 2, 2, 0, 8>(a, fwd, st);
       else launch_chain_t<64, 128, 8, 2, 2, 0>(a, fwd, st);  // (the bounds-check-free variant is 7% slower here)
       break;
@@ -782,6 +789,7 @@ void launch_chain_slice(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t s
       else if (variant == 6) launch_chain_t<128, 32, 16, 1>(a, fwd, st);
       else if (variant == 7) launch_chain_t<128, 64, 16, 1, -1, -1, 8>(a, fwd, st);
       else if (variant == 8) launch_chain_t<128, 64, 16, 1, -1, -1, 16>(a, fwd, st);
+      else if (under_wave(a, 64)) launch_chain_auto<128, 16, 16, 1>(a, fwd, st);  // narrow batches
       else launch_chain_auto<128, 64, 16, 1>(a, fwd, st);  // measured best on the c3dd interiors (+7%)
       break;
     case 256:
@@ -803,8 +811,13 @@ void launch_chain_slice(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t s
       else if (variant == 16) launch_chain_t<256, 32, 16, 1, 2, 0, 8>(a, fwd, st);
       else if (variant == 17) launch_chain_t<256, 16, 16, 1, 2, 3, 4>(a, fwd, st);
       // measured (c1, profiles/r01_chain_ab.txt): forward factor fragments 8 pair steps ahead
-      // (13.08 -> 12.74 ms; 2 ahead: 17.1 ms), 32-warp CTAs backward (-4%)
+      // (13.08 -> 12.74 ms; 2 ahead: 17.1 ms), 32-warp CTAs backward (-4%).  Narrow batches
+      // (host-pipeline chunks of 32 / 64 columns) take 8- / 16-column tiles so the chains
+      // spread over all SMs.
+      else if (fwd && under_wave(a, 16)) launch_chain_auto<256, 8, 16, 1>(a, fwd, st);
       else if (fwd) launch_chain_auto<256, 16, 16, 1, -1, -1, 8>(a, fwd, st);
+      else if (under_wave(a, 16)) launch_chain_auto<256, 8, 16, 1>(a, fwd, st);
+      else if (under_wave(a, 32)) launch_chain_auto<256, 16, 16, 1>(a, fwd, st);
       else launch_chain_auto<256, 32, 32, 1>(a, fwd, st);
       break;
     default: fail(BTD_ERR_UNSUPPORTED, "no chain kernel for this block order");

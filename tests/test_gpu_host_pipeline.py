@@ -16,9 +16,11 @@ from paper_1108_4181_b200 import BlockTriMatrix, configs, plan_build, plan_solve
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("m", [16, 64])
-@pytest.mark.parametrize("k", [64, 96, 128, 160, 256, 320])
+@pytest.mark.parametrize("m,k", [(m, k) for m in (16, 64) for k in (64, 96, 128, 160, 256, 320)]
+                         + [(128, 256), (256, 256), (256, 64), (200, 128)])
 def test_chunk_plans_match_oracle(m, k):
+    """(m = 128 / 256 / 200: narrow host chunks take narrower chain tiles so a chunk's
+    chains spread over the SMs -- every tile shape must give the oracle's answer.)"""
     n, ranks = 40, 5
     d, lo, up, f = configs.dominant_numpy(n, m, k, seed=k + m)
     plan = plan_build(BlockTriMatrix(d, lo, up), ranks)
@@ -40,3 +42,31 @@ def test_alternating_widths_reuse_plan():
         f = rng.standard_normal((n, m, k))
         x = plan_solve(plan, f)
         assert O.max_rel_err(x, O.plan_solve(oplan, f)) <= 1e-9
+
+
+def test_large_host_batches_pinned_paths():
+    """Batches >= 32 MB: the caller's buffer is page-locked on first use and reused,
+    solutions come from the pinned pool, pinned_array inputs are used as they are;
+    every path gives the same answer as the oracle, and repeated calls are bitwise equal."""
+    import paper_1108_4181_b200 as btd
+    from paper_1108_4181_b200 import _native, dichotomy
+
+    n, m, k, ranks = 512, 64, 128, 8
+    d, lo, up, f = configs.dominant_numpy(n, m, k, seed=5)
+    assert f.nbytes >= dichotomy.PIN_MIN_BYTES
+    plan = plan_build(BlockTriMatrix(d, lo, up), ranks)
+    ref = O.plan_solve(O.plan_build(d, lo, up, ranks), f)
+    x1 = plan_solve(plan, f)
+    assert O.max_rel_err(x1, ref) <= 1e-9
+    lib = _native.load()
+    import ctypes
+
+    assert lib.btd_host_is_pinned(ctypes.c_void_p(f.ctypes.data)) == 1  # registered for f's lifetime
+    assert lib.btd_host_is_pinned(ctypes.c_void_p(x1.ctypes.data)) == 1  # from the pinned pool
+    x2 = plan_solve(plan, f)
+    assert np.array_equal(x1, x2)
+    fp = btd.pinned_array(f)
+    x3 = plan_solve(plan, fp)
+    assert np.array_equal(x1, x3)
+    del x1, x2, x3
+    assert plan_solve(plan, f[:, :, :64].copy()).shape == (n, m, 64)
