@@ -248,6 +248,14 @@ class _PinnedBlock:
             pass
 
 
+def release_pinned_pool():
+    """Free the page-locked solution blocks kept for reuse (arrays still alive keep theirs)."""
+    lib = _native.load()
+    for free in _pool.values():
+        while free:
+            lib.btd_host_free(ctypes.c_void_p(free.pop()))
+
+
 def _pinned_empty(shape):
     """Uninitialised float64 C-contiguous array in page-locked memory."""
     count = int(np.prod(shape))
@@ -359,4 +367,5 @@ def plan_solve(plan, f_batch):
 
 
 __all__ = ["DevicePlan", "plan_build", "plan_build_arrays", "plan_solve", "pinned_array", "pinned_empty",
+           "release_pinned_pool",
            "BlockTriMatrix", "BlockVector"]

@@ -70,3 +70,6 @@ def test_large_host_batches_pinned_paths():
     assert np.array_equal(x1, x3)
     del x1, x2, x3
     assert plan_solve(plan, f[:, :, :64].copy()).shape == (n, m, 64)
+    assert any(dichotomy._pool.values())
+    dichotomy.release_pinned_pool()
+    assert not any(dichotomy._pool.values())
