@@ -362,12 +362,14 @@ def cpu_reference_run(name, steps=2, warmup=1, workers=None):
         for _ in range(warmup):
             rs.step()
         res = [rs.step() for _ in range(max(1, steps))]
+        one = rs.one_core_value()
     finally:
         rs.close()
     ts = [r[1] for r in res]
     value = rs.cfg["k"] * len(ts) / sum(ts) * rs.scale
     return {"value": value, "unit": "RHS/s", "cores": rs.workers, "kind": "reference", "sample": rs.sample,
-            "ms_per_step": 1e3 * sum(ts) / len(ts)}
+            "ms_per_step": 1e3 * sum(ts) / len(ts), "value_one_core": one,
+            "backend": rs.backend}
 
 
 def run_reference(args):

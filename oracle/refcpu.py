@@ -130,15 +130,27 @@ class RefSample:
                           "(solve cost is linear in N)"))
 
     def step(self):
+        """(RHS/s of the whole sample over all workers, wall seconds); the per-worker
+        solve times of the step are kept in ``last_worker_s``."""
         t0 = time.perf_counter()
         for p in self.procs:
             p.stdin.write("go\n")
             p.stdin.flush()
+        self.last_worker_s = []
         for p in self.procs:
-            if not p.stdout.readline().startswith("done"):
+            line = p.stdout.readline()
+            if not line.startswith("done"):
                 raise RuntimeError("reference worker died")
+            self.last_worker_s.append(float(line.split()[1]))
         t = time.perf_counter() - t0
         return self.cfg["k"] / t * self.scale, t
+
+    def one_core_value(self):
+        """RHS/s of ONE reference process (its columns over its own solve time), i.e. the
+        reference's single-threaded throughput on one core of this host."""
+        k = self.cfg["k"]
+        cols = [(i + 1) * k // self.workers - i * k // self.workers for i in range(self.workers)]
+        return sum(c / t for c, t in zip(cols, self.last_worker_s)) / self.workers * self.scale
 
     def close(self):
         for p in getattr(self, "procs", []):
