@@ -168,6 +168,101 @@ BTD_DEVINL void acc_store_tile(const double (&acc)[TM][TN][2], double* __restric
     }
 }
 
+// One level item (node b, 16-column tile) with everything that does not depend on the previous
+// level loaded BEFORE the grid barrier that completes it: the node's indices, its z tile and (for
+// MP <= 16, register budget) the E / H fragments.  After the barrier only the x~ fragment loads,
+// the DMMAs and the store remain on the level's critical path (c4: 11 levels, ~9 -> ~5 us each).
+template <int MP, int TM, int TN>
+struct LevelItem {
+  static constexpr bool FRAG = MP <= 16;
+  static constexpr int NS = MP / 8;
+  bool have;
+  int he, hh;
+  int64_t col0, xl, xh, kk;
+  double acc[TM][TN][2];
+  double2 ea[FRAG ? NS : 1][TM], ha[FRAG ? NS : 1][TM];
+  const double *E, *H;
+
+  // indices and factor fragments of node b
+  BTD_DEVINL void load_static(int b, int64_t c0, const int64_t* k, const int64_t* xlv, const int64_t* xhv,
+                              const int32_t* has_e, const int32_t* has_h, const double* EH, int g, int t) {
+    constexpr int64_t blk = (int64_t)MP * MP;
+    col0 = c0;
+    kk = k[b];
+    he = has_e[b];
+    hh = has_h[b];
+    xl = he ? xlv[b] : 0;
+    xh = hh ? xhv[b] : 0;
+    E = EH + (2 * (int64_t)b) * blk;
+    H = E + blk;
+    if constexpr (FRAG) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          ea[s][i] = he ? ldg_cg2(E + (i * 8 + g) * MP + 8 * s + 2 * t) : make_double2(0.0, 0.0);
+          ha[s][i] = hh ? ldg_cg2(H + (i * 8 + g) * MP + 8 * s + 2 * t) : make_double2(0.0, 0.0);
+        }
+    }
+  }
+  // acc += A x~[row] with A from the prefetched fragments (same order of sums as gmem_mma)
+  BTD_DEVINL void frag_mma(const double2 (&af)[FRAG ? NS : 1][TM], const double* __restrict__ B, int64_t K, int g,
+                           int t) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      double b0[TN], b1[TN];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const bool in = col0 + j * 8 + g < K;
+        b0[j] = in ? __ldcg(B + (int64_t)(8 * s + 2 * t) * K + j * 8 + g) : 0.0;
+        b1[j] = in ? __ldcg(B + (int64_t)(8 * s + 2 * t + 1) * K + j * 8 + g) : 0.0;
+      }
+      mma_k4<TM, TN, false>(acc, af[s], b0);
+      mma_k4<TM, TN, true>(acc, af[s], b1);
+    }
+  }
+  // x~_k = acc (= z) + E x~_{lo-1} + H x~_{hi+1}
+  BTD_DEVINL void finish(double* xt, int64_t K, int g, int t) {
+    const int64_t mpK = (int64_t)MP * K;
+    if constexpr (FRAG) {
+      if (he) frag_mma(ea, xt + xl * mpK + col0, K, g, t);
+      if (hh) frag_mma(ha, xt + xh * mpK + col0, K, g, t);
+    } else {
+      if (he) gmem_mma<MP, TM, TN>(acc, E, MP, xt + xl * mpK + col0, K, col0, K, g, t);
+      if (hh) gmem_mma<MP, TM, TN>(acc, H, MP, xt + xh * mpK + col0, K, col0, K, g, t);
+    }
+    acc_store_tile(acc, xt + kk * mpK, K, col0, g, t);
+  }
+};
+
+// acc = sum of `ncnt` consecutive partial tiles (chunk order, loads U tiles ahead)
+template <int MP, int TM, int TN>
+BTD_DEVINL void sum_partials(double (&acc)[TM][TN][2], const double* __restrict__ P0, int ncnt, int64_t K,
+                             int64_t col0, int g, int t) {
+  const int64_t mpK = (int64_t)MP * K;
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  int c = 0;
+  constexpr int U = MP <= 16 ? 4 : 2;  // loads in flight (register budget)
+  for (; c + U <= ncnt; c += U) {
+    double v[U][TM][TN][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc_load_tile(v[u], P0 + (int64_t)(c + u) * mpK, K, col0, g, t);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          acc[i][j][0] += v[u][i][j][0];
+          acc[i][j][1] += v[u][i][j][1];
+        }
+  }
+  for (; c < ncnt; ++c) acc_add_tile(acc, P0 + (int64_t)c * mpK, K, col0, g, t);
+}
+
 template <int MP>
 __global__ void __launch_bounds__(256) tree_small_kernel(TreeArgs a) {
   namespace cg = cooperative_groups;
@@ -190,45 +285,38 @@ __global__ void __launch_bounds__(256) tree_small_kernel(TreeArgs a) {
                                  a.ft + (a.lo[b] + a.ch_blk0[c]) * mpK + col0, a.ch_nblk[c], K, col0, g, t);
     acc_store_tile(acc, a.partial + (int64_t)c * mpK, K, col0, g, t);
   }
+  // phase 2: levels.  A warp's first item of level l is prepared (indices, E / H fragments, and --
+  // once the partials exist -- its z = sum of chunk partials) before the barrier that ends level l-1.
+  LevelItem<MP, TM, TN> it;
+  int itb = 0;
+  auto prep_static = [&](int l) {
+    const int n0 = a.lv_off[l], n1 = a.lv_off[l + 1];
+    it.have = gw < (n1 - n0) * ntile;
+    if (it.have) {
+      itb = a.lv_nodes[n0 + gw / ntile];
+      it.load_static(itb, (int64_t)(gw % ntile) * 16, a.k, a.xl, a.xh, a.has_e, a.has_h, a.EH, g, t);
+    }
+  };
+  auto prep_z = [&]() {
+    if (it.have)
+      sum_partials<MP, TM, TN>(it.acc, a.partial + (int64_t)a.zc_off[itb] * mpK, a.zc_cnt[itb], K, it.col0, g, t);
+  };
+  if (a.nlev > 0) prep_static(0);
   grid.sync();
-  // phase 2: levels
+  if (a.nlev > 0) prep_z();
   for (int l = 0; l < a.nlev; ++l) {
     const int n0 = a.lv_off[l], n1 = a.lv_off[l + 1];
-    for (int item = gw; item < (n1 - n0) * ntile; item += nw) {
+    if (it.have) it.finish(a.xt, K, g, t);
+    for (int item = gw + nw; item < (n1 - n0) * ntile; item += nw) {  // further items of a wide level
+      LevelItem<MP, TM, TN> o;
       const int b = a.lv_nodes[n0 + item / ntile];
-      const int64_t col0 = (int64_t)(item % ntile) * 16;
-      double acc[TM][TN][2];
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-      {  // partial sums in chunk order, loads U chunks ahead
-        const double* P0 = a.partial + (int64_t)a.zc_off[b] * mpK;
-        const int ncnt = a.zc_cnt[b];
-        int c = 0;
-        constexpr int U = MP <= 16 ? 4 : 2;  // loads in flight (register budget)
-        for (; c + U <= ncnt; c += U) {
-          double v[U][TM][TN][2];
-#pragma unroll
-          for (int u = 0; u < U; ++u) acc_load_tile(v[u], P0 + (int64_t)(c + u) * mpK, K, col0, g, t);
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int i = 0; i < TM; ++i)
-#pragma unroll
-              for (int j = 0; j < TN; ++j) {
-                acc[i][j][0] += v[u][i][j][0];
-                acc[i][j][1] += v[u][i][j][1];
-              }
-        }
-        for (; c < ncnt; ++c) acc_add_tile(acc, P0 + (int64_t)c * mpK, K, col0, g, t);
-      }
-      if (a.has_e[b])
-        gmem_mma<MP, TM, TN>(acc, a.EH + (2 * (int64_t)b) * blk, MP, a.xt + a.xl[b] * mpK + col0, K, col0, K, g, t);
-      if (a.has_h[b])
-        gmem_mma<MP, TM, TN>(acc, a.EH + (2 * (int64_t)b + 1) * blk, MP, a.xt + a.xh[b] * mpK + col0, K, col0, K, g,
-                             t);
-      acc_store_tile(acc, a.xt + a.k[b] * mpK, K, col0, g, t);
+      o.load_static(b, (int64_t)(item % ntile) * 16, a.k, a.xl, a.xh, a.has_e, a.has_h, a.EH, g, t);
+      sum_partials<MP, TM, TN>(o.acc, a.partial + (int64_t)a.zc_off[b] * mpK, a.zc_cnt[b], K, o.col0, g, t);
+      o.finish(a.xt, K, g, t);
+    }
+    if (l + 1 < a.nlev) {
+      prep_static(l + 1);
+      prep_z();
     }
     grid.sync();
   }
@@ -337,20 +425,30 @@ __global__ void __launch_bounds__(256) tree_shard_c_kernel(ShardTreeArgs a) {
     }
     grid.sync();
   }
+  // levels, a warp's first item of level l prepared before the barrier that ends level l-1 (as in
+  // tree_small_kernel); z of a crossing node exists only after the barrier above
+  LevelItem<MP, TM, TN> it;
+  auto prep = [&](int l, bool with_z) {
+    const int n0 = a.lv_off[l], n1 = a.lv_off[l + 1];
+    it.have = gw < (n1 - n0) * ntile;
+    if (it.have) {
+      const int b = a.lv_nodes[n0 + gw / ntile];
+      it.load_static(b, (int64_t)(gw % ntile) * 16, a.k, a.xl, a.xh, a.has_e, a.has_h, a.EH, g, t);
+      if (with_z) acc_load_tile(it.acc, a.z + (int64_t)b * mpK, K, it.col0, g, t);
+    }
+  };
+  if (a.nlev > 0) prep(0, true);
   for (int l = 0; l < a.nlev; ++l) {
     const int n0 = a.lv_off[l], n1 = a.lv_off[l + 1];
-    for (int item = gw; item < (n1 - n0) * ntile; item += nw) {
+    if (it.have) it.finish(a.xt, K, g, t);
+    for (int item = gw + nw; item < (n1 - n0) * ntile; item += nw) {
+      LevelItem<MP, TM, TN> o;
       const int b = a.lv_nodes[n0 + item / ntile];
-      const int64_t col0 = (int64_t)(item % ntile) * 16;
-      double acc[TM][TN][2];
-      acc_load_tile(acc, a.z + (int64_t)b * mpK, K, col0, g, t);
-      if (a.has_e[b])
-        gmem_mma<MP, TM, TN>(acc, a.EH + (2 * (int64_t)b) * blk, MP, a.xt + a.xl[b] * mpK + col0, K, col0, K, g, t);
-      if (a.has_h[b])
-        gmem_mma<MP, TM, TN>(acc, a.EH + (2 * (int64_t)b + 1) * blk, MP, a.xt + a.xh[b] * mpK + col0, K, col0, K, g,
-                             t);
-      acc_store_tile(acc, a.xt + a.k[b] * mpK, K, col0, g, t);
+      o.load_static(b, (int64_t)(item % ntile) * 16, a.k, a.xl, a.xh, a.has_e, a.has_h, a.EH, g, t);
+      acc_load_tile(o.acc, a.z + (int64_t)b * mpK, K, o.col0, g, t);
+      o.finish(a.xt, K, g, t);
     }
+    if (l + 1 < a.nlev) prep(l + 1, true);
     grid.sync();
   }
 }
