@@ -500,12 +500,14 @@ def run_b200(args):
         plan = plan_build_arrays(diag, lower, upper, ranks, split=split)
         row_lo, row_hi = 0, n
         nranges, L, mode, fbytes = plan.nranges, plan.L, plan.mode, plan.factor_bytes
+        scoup = bool(plan.scalar_coupling)
         handle = plan.handle
     else:
         plan = ShardedPlan(diag, lower, upper, ranks, split=split)
         row_lo, row_hi = plan.row_lo, plan.row_hi
         info = plan.be.info(plan.h)
         nranges, L, mode, fbytes = plan.nranges, plan.L, int(info.mode), int(info.factor_bytes)
+        scoup = bool(info.scalar_coupling)
         handle = plan.h
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
@@ -650,10 +652,13 @@ def run_b200(args):
     hbm = float(pk.get("hbm_gbs", 6650.0))
     fp64 = fp64_peak_tflops(torch)
     nint = interior_rows(n, nranges, L) / world
-    fwd_flops = 6.0 * m * m * K * nint
-    fwd_bytes = 8.0 * (3 * m * m + 2 * m * K) * nint
-    tot_flops = 10.0 * m * m * K * n / world
-    tot_bytes = 8.0 * (5 * m * m + 4 * m * K) * n / world
+    # scalar-coupled plans (interior lower blocks a I: c1) run the forward sweep with two block
+    # products per row instead of three: 4 M^2 K flops and two factor streams
+    fprod = 2 if scoup else 3
+    fwd_flops = 2.0 * fprod * m * m * K * nint
+    fwd_bytes = 8.0 * (fprod * m * m + 2 * m * K) * nint
+    tot_flops = 2.0 * (fprod + 2) * m * m * K * n / world
+    tot_bytes = 8.0 * ((fprod + 2) * m * m + 4 * m * K) * n / world
     hbm_bound = tot_flops / (fp64 * 1e12) < tot_bytes / (hbm * 1e9)
     t_fwd = ph[0] / 1e3
     if hbm_bound:
@@ -662,10 +667,11 @@ def run_b200(args):
         roof = {"bound": "tensor", "achieved": fwd_flops / t_fwd / 1e12, "peak": fp64, "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = ncu_traffic(name)
-    roof["kernel"] = (("stream_fwd_kernel (TMA bulk-copy ring)" if m <= 32 and K % 2 == 0 else "chain_fwd_kernel")
+    roof["kernel"] = (("stream_fwd_kernel (TMA bulk-copy ring)" if m <= 32 and K % 2 == 0 else
+                       "chain_fwd_sc_kernel (scalar-coupled: 2 products per row)" if scoup else "chain_fwd_kernel")
                       if mode == 0 else "gemm_tma_kernel (mode 1: one batched TMA GEMM per row step)")
-    roof["algorithmic_per_launch"] = (f"{fwd_bytes:.4e} B = 8(3M^2+2MK) x {nint:.0f} interior rows" if hbm_bound
-                                      else f"{fwd_flops:.4e} flop = 6M^2K x {nint:.0f} interior rows")
+    roof["algorithmic_per_launch"] = (f"{fwd_bytes:.4e} B = 8({fprod}M^2+2MK) x {nint:.0f} interior rows" if hbm_bound
+                                      else f"{fwd_flops:.4e} flop = {2 * fprod}M^2K x {nint:.0f} interior rows")
     roof["peak_source"] = ("cuBLAS DGEMM 4096^3 measured in this run (fp64 tensor; MEASURED_PEAKS.json has no fp64)"
                            if not hbm_bound else "MEASURED_PEAKS.json hbm_gbs (burst copy)")
     t_roof = max(tot_flops / (fp64 * 1e12), tot_bytes / (hbm * 1e9))
@@ -689,7 +695,7 @@ def run_b200(args):
         "data": "synthetic (seeded numpy stream of configs.generate, BASELINE.json distributions; "
                 "identical to the reference's full-size golden inputs)",
         "config": {"workload": name, "n": n, "m": m, "k": K, "ranks": ranks, "split": split,
-                   "device_ranges": nranges, "L": L, "mode": mode,
+                   "device_ranges": nranges, "L": L, "mode": mode, "scalar_coupling": scoup,
                    "parallelism": f"rows sharded over {world} GPUs (NCCL all-gather of interface pairs)"
                    if sharded else "single GPU",
                    "l2": "inputs larger than L2 (F %.2f GB, factors %.2f GB per GPU)" % (
@@ -810,7 +816,8 @@ def run_dd(args):
     res = dd.residual(x, f)
     fp64 = fp64_peak_tflops(torch)
     ni = [e - a for a, e in dd.sub]
-    flops = 2 * sum(10.0 * nx * n * n * K for n in ni) + 10.0 * (nsub - 1) * nx * nx * K
+    ifl = 8.0 if all(getattr(p, "scalar_coupling", False) for p in dd.plans) else 10.0  # scalar-coupled interiors
+    flops = 2 * sum(ifl * nx * n * n * K for n in ni) + 10.0 * (nsub - 1) * nx * nx * K
     line = {"metric": "rhs_columns_per_second", "value": K / (ms / 1e3), "unit": "RHS/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "none", "vs_baseline": None, "dtype": "f64",
@@ -819,8 +826,8 @@ def run_dd(args):
                        "interior_ranks": dd.plans[0].nranges},
             "solve_roofline": {"flops": flops, "t_roof_ms": flops / (fp64 * 1e12) * 1e3,
                                "frac": flops / (fp64 * 1e12) * 1e3 / ms, "fp64_tflops_peak": fp64},
-            "plan_build_s": build_s,
-        "plan_build_warm_s": build_warm_s, "grid_rel_residual": res, "clocks": clk.summary(),
+            "plan_build_s": build_s, "scalar_coupled_interiors": ifl == 8.0,
+            "grid_rel_residual": res, "clocks": clk.summary(),
             "gpu_launches": _native.launch_count() - lc0}
     emit(line)
 

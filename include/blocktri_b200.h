@@ -60,6 +60,9 @@ typedef struct btd_plan_info {
   int32_t mode;              /* 0 = fused chain kernels, 1 = per-step GEMM sweep (large m) */
   int32_t rank, world;       /* shard of a row-sharded plan (0, 1 when not sharded) */
   int64_t range_lo, range_hi;/* device ranges owned by this shard */
+  int64_t scalar_coupling;   /* 1: every interior lower block is a scalar multiple of I (5-point-stencil
+                              * operators); the forward sweep then runs y_j = Dinv_j (f_j + a_j y_{j-1}):
+                              * 8 instead of 10 M^2 K flops per row and batch.  BTD_SCALAR_COUPLING=0 disables. */
 } btd_plan_info;
 
 /* Algorithm 2 step 1 (ref dichotomy.py:318-338): validate 1 <= ranks <= n

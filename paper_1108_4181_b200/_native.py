@@ -71,6 +71,7 @@ class PlanInfo(ctypes.Structure):
         ("device", ctypes.c_int32), ("mode", ctypes.c_int32),
         ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
         ("range_lo", ctypes.c_int64), ("range_hi", ctypes.c_int64),
+        ("scalar_coupling", ctypes.c_int64),
     ]
 
 

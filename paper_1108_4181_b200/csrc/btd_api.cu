@@ -100,6 +100,26 @@ struct DevBuf {
   int32_t* i32() const { return static_cast<int32_t*>(p); }
 };
 
+// Scalar-coupling probe: slot s = (range q, interior row j) -> is the row's lower block a I
+// (exactly)?  alpha[s] = a; *bad set when any live slot's block is not.
+__global__ void scalar_coupling_kernel(const double* Lw, const int64_t* lo, const int32_t* nint, int64_t cap, int mp,
+                                       double* alpha, int* bad) {
+  const int64_t s = blockIdx.x, q = s / cap, j = s % cap;
+  if (j >= nint[q]) {
+    if (threadIdx.x == 0) alpha[s] = 0.0;
+    return;
+  }
+  const double* B = Lw + (lo[q] + j) * (int64_t)mp * mp;
+  const double d = B[0];
+  bool ok = true;
+  for (int e = threadIdx.x; e < mp * mp; e += blockDim.x) {
+    const double v = B[e];
+    if (e / mp == e % mp ? !(v == d) : !(v == 0.0)) ok = false;
+  }
+  if (!ok) *bad = 1;
+  if (threadIdx.x == 0) alpha[s] = d;
+}
+
 __global__ void pad_blocks_kernel(const double* src, int64_t nsrc, int m, double* dst, int64_t ndst,
                                   int mp, int diag_identity) {
   const int64_t total = ndst * mp * mp;
@@ -363,6 +383,10 @@ struct btd_plan {
   const int32_t* d_nint = nullptr;
   DevBuf pool;     // local factor blocks + global reduced blocks
   DevBuf contrib;  // [nrl][4][mp][mp]: C_lo - B_lo U[1],  A V_last,  A U_last,  B_lo V[1]
+  // scalar-coupled plan (every interior lower block a_g I, m == mp, chain kernels): the forward
+  // sweep runs y_j = Dinv_j (f_g + a_g y_{j-1}) with Tbd_j = Tb_j Dinv_j (chain_fwd_sc_kernel)
+  int scoup = 0;
+  int64_t off_Tbd = 0, off_al = 0;
   int64_t off_AD = 0, off_Dinv = 0, off_S = 0, off_G = 0, off_Tb = 0, off_Fc = 0, off_Bif = 0,
           off_BU = 0, off_BV = 0, off_Dt = 0, off_Rd = 0, off_Rl = 0, off_Ru = 0, off_RdT = 0,
           off_RlT = 0, off_RuT = 0, off_Z = 0, off_I = 0;
@@ -667,6 +691,22 @@ void launch_chain_t(const ChainArgs& a, bool fwd, cudaStream_t st) {
   CK_LAUNCH();
 }
 
+// Forward sweep of a scalar-coupled plan (chain_fwd_sc_kernel): chain state + two F tiles.
+template <int MP, int KT, int WR, int WC, int PF = -1>
+void launch_chain_sc(const ChainArgs& a, cudaStream_t st) {
+  using Cfg = ChainCfg<MP, KT, WR, WC, 2, -1, PF>;
+  const size_t smem = (size_t)3 * MP * Cfg::LD * sizeof(double);
+  dim3 grid((unsigned)((a.K + KT - 1) / KT), (unsigned)a.nr);
+  if (a.m == MP && a.K % KT == 0 && a.K % 2 == 0) {
+    set_smem_attr((const void*)chain_fwd_sc_kernel<MP, KT, WR, WC, 2, -1, PF, 1, 1>, smem);
+    chain_fwd_sc_kernel<MP, KT, WR, WC, 2, -1, PF, 1, 1><<<grid, Cfg::NT, smem, st>>>(a);
+  } else {
+    set_smem_attr((const void*)chain_fwd_sc_kernel<MP, KT, WR, WC, 2, -1, PF, 1, 0>, smem);
+    chain_fwd_sc_kernel<MP, KT, WR, WC, 2, -1, PF, 1, 0><<<grid, Cfg::NT, smem, st>>>(a);
+  }
+  CK_LAUNCH();
+}
+
 // Default shapes: a bounds-check-free variant when every tile is full (block order == MP,
 // K a multiple of the column tile, K even).
 template <int MP, int KT, int WR, int WC, int NF = -1, int NY = -1, int PF = -1>
@@ -746,6 +786,32 @@ void launch_chain_slice(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t s
     variant_b = eb ? atoi(eb) : variant_f;
   }
   const int variant = fwd ? variant_f : variant_b;
+  if (fwd && a.Tbd) {  // scalar-coupled plan: the two-product forward sweep (same tile policy as below)
+    static int scv = -1;
+    if (scv < 0) {
+      const char* e = getenv("BTD_SC_VARIANT");
+      scv = e ? atoi(e) : 0;
+    }
+    switch (mp) {
+      case 64:
+        if (under_wave(a, 128)) launch_chain_sc<64, 32, 8, 1>(a, st);
+        else launch_chain_sc<64, 128, 8, 2, 8>(a, st);
+        return;
+      case 128:
+        if (under_wave(a, 64)) launch_chain_sc<128, 16, 16, 1>(a, st);
+        else launch_chain_sc<128, 64, 16, 1>(a, st);
+        return;
+      case 256:
+        if (scv == 1) launch_chain_sc<256, 32, 16, 1, 4>(a, st);
+        else if (scv == 2) launch_chain_sc<256, 32, 32, 1>(a, st);
+        else if (scv == 3) launch_chain_sc<256, 16, 16, 1, 4>(a, st);
+        else if (scv == 4) launch_chain_sc<256, 32, 16, 1, 8>(a, st);
+        else if (under_wave(a, 16)) launch_chain_sc<256, 8, 16, 1>(a, st);
+        else launch_chain_sc<256, 16, 16, 1, 8>(a, st);
+        return;
+      default: fail(BTD_ERR_UNSUPPORTED, "scalar-coupled plan: no forward kernel for this block order");
+    }
+  }
   switch (mp) {
     case 8: launch_chain_t<8, 32, 1, 4>(a, fwd, st); break;
     case 16: launch_chain_t<16, 16, 1, 1>(a, fwd, st); break;
@@ -901,6 +967,28 @@ void build_local(btd_plan& pl, const double* diag, const double* lower, const do
   tmp.release();
   const double* Cm = mat.d();
   const int64_t offL = nl, offU = 2 * nl;
+  DevBuf sc_alpha;
+  if (restore < 0) {
+    static int sc_on = -1;
+    if (sc_on < 0) {
+      const char* e = getenv("BTD_SCALAR_COUPLING");
+      sc_on = e ? atoi(e) : 1;
+    }
+    pl.scoup = 0;
+    if (sc_on && pl.mode == 0 && m == mp && mp >= 64 && cap > 0 && nrl > 0) {
+      DevBuf bad;
+      bad.alloc(sizeof(int));
+      sc_alpha.alloc((size_t)nrl * cap * sizeof(double));
+      CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+      scalar_coupling_kernel<<<(unsigned)(nrl * cap), 256, 0, st>>>(Cm + offL * blk, pl.d_lo, pl.d_nint, cap, (int)mp,
+                                                                 sc_alpha.d(), static_cast<int*>(bad.p));
+      CK_LAUNCH();
+      int hbad = 1;
+      CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      pl.scoup = hbad ? 0 : 1;
+    }
+  }
 
   // ---- pool layout: local factors, global reduced system, constants
   const int64_t nslot = nrl * cap;
@@ -924,6 +1012,12 @@ void build_local(btd_plan& pl, const double* diag, const double* lower, const do
   pl.off_RuT = take(nr);
   pl.off_Z = take(1);
   pl.off_I = take(1);
+  if (pl.scoup) {
+    // Tbd takes over the AD section once the build no longer needs AD (a scalar-coupled plan never
+    // runs the general forward sweep: launch_chain_slice covers every shape with chain_fwd_sc_kernel)
+    pl.off_Tbd = pl.off_AD;
+    pl.off_al = take((nslot + blk - 1) / blk);  // a_g per slot, as doubles inside the pool (plan images carry it)
+  }
   pl.pool.alloc((size_t)o * blk * sizeof(double));
   CK(cudaMemsetAsync(pl.pool.p, 0, (size_t)o * blk * sizeof(double), st));
   set_identity_kernel<<<64, 256, 0, st>>>(pl.P(pl.off_I), (int)mp);
@@ -1006,6 +1100,12 @@ void build_local(btd_plan& pl, const double* diag, const double* lower, const do
                 {term(mk(pool, slot_arr, pl.off_Tb + cap - 1, blk, mp), mk(pool, slot_arr, pl.off_S + cap - 1, blk, mp),
                       mp)},
                 st);
+    if (pl.scoup) {  // Tbd_s = Tb_s Dinv_s for every slot, over AD (G_j = AD_j G_{j-1} is done); a_g beside it
+      launch_gemm(mp, mp, (int)nslot, mk(pool, nullptr, pl.off_Tbd, blk, mp), none(), 0.0,
+                  {term(mk(pool, nullptr, pl.off_Tb, blk, mp), mk(pool, nullptr, pl.off_Dinv, blk, mp), mp)}, st);
+      CK(cudaMemcpyAsync(pool + pl.off_al * blk, sc_alpha.p, (size_t)nslot * sizeof(double), cudaMemcpyDeviceToDevice,
+                         st));
+    }
   }
 
   // ---- range failures: first range (in order) wins, row local to its interior
@@ -1601,6 +1701,8 @@ ChainArgs chain_args(btd_plan& pl, const double* F, double* X, int64_t K, double
   a.S = pool + pl.off_S * blk; a.G = pool + pl.off_G * blk;
   a.base = base; a.base_stride = base_stride;
   a.xt = pl.S().xt.d() + pl.q0 * pl.mp * K;
+  a.Tbd = pl.scoup ? pool + pl.off_Tbd * blk : nullptr;
+  a.alpha = pl.scoup ? pool + pl.off_al * blk : nullptr;
   return a;
 }
 
@@ -2461,8 +2563,9 @@ int btd_plan_export(btd_plan* pl, void* dst, int64_t* nbytes, void* stream) {
   if (*nbytes < need) { g_err = "btd_plan_export: destination too small"; return BTD_ERR_INVALID_ARG; }
   *nbytes = need;
   return guarded(pl, stream, [&](cudaStream_t st) {
+    // mode field: sweep mode in the low byte, the scalar-coupling flag (extra pool sections) above it
     ImageHeader h{kImageMagic, kImageVersion, pl->n, pl->m, pl->ranks, pl->split, pl->rank, pl->world,
-                  pl->mode, pl->mp, (int64_t)pl->pool.bytes, (int64_t)pl->Rrows.bytes, (int64_t)pl->EH.bytes};
+                  pl->mode | (pl->scoup << 8), pl->mp, (int64_t)pl->pool.bytes, (int64_t)pl->Rrows.bytes, (int64_t)pl->EH.bytes};
     char* out = static_cast<char*>(dst);
     memcpy(out, &h, sizeof h);
     out += sizeof h;
@@ -2485,7 +2588,8 @@ int btd_plan_import(const void* src, int64_t nbytes, int device, void* stream, b
   if (h.magic != kImageMagic) { g_err = "plan image: bad magic"; return BTD_ERR_INVALID_ARG; }
   if (h.version != kImageVersion) { g_err = "plan image: unsupported version"; return BTD_ERR_UNSUPPORTED; }
   if (h.n < 1 || h.m < 1 || h.ranks < 1 || h.ranks > h.n || h.split < 1 || h.world < 1 || h.rank < 0 ||
-      h.rank >= h.world || (h.mode != 0 && h.mode != 1) || h.pool_bytes < 0 || h.rrows_bytes < 0 || h.eh_bytes < 0 ||
+      h.rank >= h.world || ((h.mode & 0xff) != 0 && (h.mode & 0xff) != 1) || (h.mode >> 8) < 0 || (h.mode >> 8) > 1 ||
+      h.pool_bytes < 0 || h.rrows_bytes < 0 || h.eh_bytes < 0 ||
       nbytes != (int64_t)sizeof h + h.pool_bytes + h.rrows_bytes + h.eh_bytes) {
     g_err = "plan image: inconsistent header or size";
     return BTD_ERR_INVALID_ARG;
@@ -2498,7 +2602,8 @@ int btd_plan_import(const void* src, int64_t nbytes, int device, void* stream, b
     DeviceGuard dg(device);
     cudaStream_t st = (cudaStream_t)stream;
     int64_t row = -1, rng = -1;
-    build_local(*pl, nullptr, nullptr, nullptr, 0, st, &row, &rng, (int)h.mode);
+    pl->scoup = (int)(h.mode >> 8);
+    build_local(*pl, nullptr, nullptr, nullptr, 0, st, &row, &rng, (int)(h.mode & 0xff));
     if (pl->mp != h.mp || (int64_t)pl->pool.bytes != h.pool_bytes) fail(BTD_ERR_INVALID_ARG, "plan image: pool layout mismatch");
     const char* in = static_cast<const char*>(src) + sizeof h;
     CK(cudaMemcpyAsync(pl->pool.p, in, h.pool_bytes, cudaMemcpyHostToDevice, st));
@@ -2567,6 +2672,7 @@ int btd_plan_query(const btd_plan* pl, btd_plan_info* info) {
   info->row_lo = pl->R0; info->row_hi = pl->R0 + pl->nloc;
   info->device = pl->device; info->mode = pl->mode;
   info->rank = pl->rank; info->world = pl->world; info->range_lo = pl->q0; info->range_hi = pl->q1;
+  info->scalar_coupling = pl->scoup;
   return BTD_OK;
 }
 

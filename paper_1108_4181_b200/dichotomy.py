@@ -103,6 +103,8 @@ class DevicePlan:
         self.nranges = int(info.nranges)
         self.npad = self.L * self.nranges
         self.mode = int(info.mode)
+        # every interior lower coupling is a scalar multiple of I: two-product forward sweep (8 M^2 K flops per row)
+        self.scalar_coupling = bool(info.scalar_coupling)
         self.factor_bytes = int(info.factor_bytes)
         self.tree_depth = int(info.tree_depth)
 

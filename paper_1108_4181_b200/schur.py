@@ -175,8 +175,10 @@ class HelmholtzDD:
       block-per-x-column orientation (acoustic.py:231-243): nx block rows of
       order n_i <= Mi with C = tridiag(-1, 4 + s_z, -1) over z and A = B = I.
       ``groups`` plans each stack nsub/groups subdomains (zero couplings between
-      them, blocks identity-padded to Mi) -- every A_ii^{-1} of a group is ONE
-      dichotomy solve.
+      them; shorter subdomains padded to order Mi by a decoupled tridiag(-1, 4, -1)
+      chain with zero right-hand sides, so every coupling block stays I -- a
+      scalar-coupled plan, two-product forward sweep) -- every A_ii^{-1} of a
+      group is ONE dichotomy solve.
     * Interface: the explicit S (schur_blocks_torch) solved by its own plan.
     * solve(f): f (nz, nx, K) on the device -> x (nz, nx, K).
     """
@@ -211,8 +213,8 @@ class HelmholtzDD:
                                                                              device=device), 1) \
                     - torch.diag(torch.ones(ni - 1, dtype=torch.float64, device=device), -1)
                 diag[j, :ni, :ni] = d
-                diag[j, ni:, ni:] = torch.eye(Mi - ni, dtype=torch.float64, device=device)
-                eye[j, :ni, :ni] = torch.eye(ni, dtype=torch.float64, device=device)
+                diag[j, ni:, ni:] = 4.0 * torch.eye(Mi - ni, dtype=torch.float64, device=device)
+                eye[j] = torch.eye(Mi, dtype=torch.float64, device=device)
             D = diag.repeat_interleave(nx, dim=0).contiguous()
             cpl = eye.repeat_interleave(nx, dim=0)[: n - 1].clone()
             cpl[nx - 1::nx] = 0.0  # no coupling across subdomain boundaries
@@ -232,7 +234,7 @@ class HelmholtzDD:
         out = torch.empty((per * self.nx, self.Mi, K), dtype=torch.float64, device=f.device)
         for j, (a, e) in enumerate(self.sub[gidx * per:(gidx + 1) * per]):
             out[j * self.nx:(j + 1) * self.nx, : e - a] = f[a:e].permute(1, 0, 2)
-            if e - a < self.Mi:  # identity-padded rows of shorter subdomains (no full zero fill)
+            if e - a < self.Mi:  # padding rows of shorter subdomains: zero right-hand side (no full zero fill)
                 out[j * self.nx:(j + 1) * self.nx, e - a:] = 0.0
         return out
 
