@@ -692,17 +692,17 @@ void launch_chain_t(const ChainArgs& a, bool fwd, cudaStream_t st) {
 }
 
 // Forward sweep of a scalar-coupled plan (chain_fwd_sc_kernel): chain state + two F tiles.
-template <int MP, int KT, int WR, int WC, int PF = -1>
-void launch_chain_sc(const ChainArgs& a, cudaStream_t st) {
+template <int MP, int KT, int WR, int WC, int PF = -1, int MINB = 1>
+void launch_chain_sc(const ChainArgsSc& a, cudaStream_t st) {
   using Cfg = ChainCfg<MP, KT, WR, WC, 2, -1, PF>;
   const size_t smem = (size_t)3 * MP * Cfg::LD * sizeof(double);
   dim3 grid((unsigned)((a.K + KT - 1) / KT), (unsigned)a.nr);
   if (a.m == MP && a.K % KT == 0 && a.K % 2 == 0) {
-    set_smem_attr((const void*)chain_fwd_sc_kernel<MP, KT, WR, WC, 2, -1, PF, 1, 1>, smem);
-    chain_fwd_sc_kernel<MP, KT, WR, WC, 2, -1, PF, 1, 1><<<grid, Cfg::NT, smem, st>>>(a);
+    set_smem_attr((const void*)chain_fwd_sc_kernel<MP, KT, WR, WC, 2, -1, PF, MINB, 1>, smem);
+    chain_fwd_sc_kernel<MP, KT, WR, WC, 2, -1, PF, MINB, 1><<<grid, Cfg::NT, smem, st>>>(a);
   } else {
-    set_smem_attr((const void*)chain_fwd_sc_kernel<MP, KT, WR, WC, 2, -1, PF, 1, 0>, smem);
-    chain_fwd_sc_kernel<MP, KT, WR, WC, 2, -1, PF, 1, 0><<<grid, Cfg::NT, smem, st>>>(a);
+    set_smem_attr((const void*)chain_fwd_sc_kernel<MP, KT, WR, WC, 2, -1, PF, MINB, 0>, smem);
+    chain_fwd_sc_kernel<MP, KT, WR, WC, 2, -1, PF, MINB, 0><<<grid, Cfg::NT, smem, st>>>(a);
   }
   CK_LAUNCH();
 }
@@ -757,11 +757,12 @@ bool launch_stream(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
 // True when a KT-column tiling of this batch fills less than one wave of 148 SMs.
 bool under_wave(const ChainArgs& a, int kt) { return (int64_t)a.nr * ((a.K + kt - 1) / kt) < 148; }
 
-void launch_chain_slice(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st);
+struct ScPools { const double* Tbd; const double* alpha; };  // scalar-coupled plan: forward-sweep extras
+void launch_chain_slice(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st, const ScPools* sc);
 
 // Sweep kernels index ranges by blockIdx.y (at most 65535): more ranges (ranks * split up to
 // N) run as consecutive slices with the per-range arrays and outputs offset.
-void launch_chain(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
+void launch_chain(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st, const ScPools* sc = nullptr) {
   constexpr int kMaxY = 65535;
   for (int q0 = 0; q0 < a.nr; q0 += kMaxY) {
     ChainArgs s = a;
@@ -771,11 +772,12 @@ void launch_chain(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
     s.slot0 = a.slot0 + q0;
     if (a.base) s.base = a.base + (int64_t)q0 * a.base_stride;
     if (a.xt) s.xt = a.xt + (int64_t)q0 * mp * a.K;
-    launch_chain_slice(mp, s, fwd, st);
+    launch_chain_slice(mp, s, fwd, st, sc);
   }
 }
 
-void launch_chain_slice(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t st) {
+void launch_chain_slice(int64_t mp, const ChainArgs& a0, bool fwd, cudaStream_t st, const ScPools* sc) {
+  const ChainArgs& a = a0;
   if (a.nr <= 0) return;
   if (launch_stream(mp, a, fwd, st)) return;
   static int variant_f = -1, variant_b = -1;
@@ -786,7 +788,11 @@ void launch_chain_slice(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t s
     variant_b = eb ? atoi(eb) : variant_f;
   }
   const int variant = fwd ? variant_f : variant_b;
-  if (fwd && a.Tbd) {  // scalar-coupled plan: the two-product forward sweep (same tile policy as below)
+  if (fwd && sc) {  // scalar-coupled plan: the two-product forward sweep (same tile policy as below)
+    ChainArgsSc as;
+    static_cast<ChainArgs&>(as) = a0;
+    as.Tbd = sc->Tbd;
+    as.alpha = sc->alpha;
     static int scv = -1;
     if (scv < 0) {
       const char* e = getenv("BTD_SC_VARIANT");
@@ -794,20 +800,20 @@ void launch_chain_slice(int64_t mp, const ChainArgs& a, bool fwd, cudaStream_t s
     }
     switch (mp) {
       case 64:
-        if (under_wave(a, 128)) launch_chain_sc<64, 32, 8, 1>(a, st);
-        else launch_chain_sc<64, 128, 8, 2, 8>(a, st);
+        if (under_wave(a, 128)) launch_chain_sc<64, 32, 8, 1>(as, st);
+        else launch_chain_sc<64, 128, 8, 2, 8>(as, st);
         return;
       case 128:
-        if (under_wave(a, 64)) launch_chain_sc<128, 16, 16, 1>(a, st);
-        else launch_chain_sc<128, 64, 16, 1>(a, st);
+        if (under_wave(a, 64)) launch_chain_sc<128, 16, 16, 1>(as, st);
+        else launch_chain_sc<128, 64, 16, 1>(as, st);
         return;
       case 256:
-        if (scv == 1) launch_chain_sc<256, 32, 16, 1, 4>(a, st);
-        else if (scv == 2) launch_chain_sc<256, 32, 32, 1>(a, st);
-        else if (scv == 3) launch_chain_sc<256, 16, 16, 1, 4>(a, st);
-        else if (scv == 4) launch_chain_sc<256, 32, 16, 1, 8>(a, st);
-        else if (under_wave(a, 16)) launch_chain_sc<256, 8, 16, 1>(a, st);
-        else launch_chain_sc<256, 16, 16, 1, 8>(a, st);
+        if (scv == 1) launch_chain_sc<256, 32, 16, 1, 4>(as, st);
+        else if (scv == 2) launch_chain_sc<256, 32, 32, 1>(as, st);
+        else if (scv == 3) launch_chain_sc<256, 16, 16, 1, 4>(as, st);
+        else if (scv == 4) launch_chain_sc<256, 32, 16, 1, 8>(as, st);
+        else if (under_wave(a, 16)) launch_chain_sc<256, 8, 16, 1>(as, st);
+        else launch_chain_sc<256, 16, 16, 1, 8>(as, st);
         return;
       default: fail(BTD_ERR_UNSUPPORTED, "scalar-coupled plan: no forward kernel for this block order");
     }
@@ -1701,8 +1707,6 @@ ChainArgs chain_args(btd_plan& pl, const double* F, double* X, int64_t K, double
   a.S = pool + pl.off_S * blk; a.G = pool + pl.off_G * blk;
   a.base = base; a.base_stride = base_stride;
   a.xt = pl.S().xt.d() + pl.q0 * pl.mp * K;
-  a.Tbd = pl.scoup ? pool + pl.off_Tbd * blk : nullptr;
-  a.alpha = pl.scoup ? pool + pl.off_al * blk : nullptr;
   return a;
 }
 
@@ -1713,7 +1717,8 @@ void solve_forward(btd_plan& pl, const double* F, double* X, int64_t K, double* 
   const int64_t mK = m * K;
   double* pool = pl.pool.d();
   if (pl.mode == 0) {  // each CTA owns its (rows, columns): in-place F == X is safe
-    launch_chain(mp, chain_args(pl, F, X, K, base, base_stride), true, st);
+    const ScPools scp{pool + pl.off_Tbd * blk, pool + pl.off_al * blk};
+    launch_chain(mp, chain_args(pl, F, X, K, base, base_stride), true, st, pl.scoup ? &scp : nullptr);
     return;
   }
   // mode 1: a step's GEMM reads all of F[g] as its reduction operand while other

@@ -39,7 +39,12 @@ struct ChainArgs {
   double* base;          // fwd out: range q at base + q*base_stride ([MP][K] each)
   int64_t base_stride;
   const double* xt;      // bwd in:  [nr+1][MP][K], range q uses blocks q and q+1
-  // scalar-coupled plans (interior lower blocks A_g = a_g I; nullptr otherwise):
+};
+
+// Forward sweep of a scalar-coupled plan (interior lower blocks A_g = a_g I).  A separate
+// parameter struct: growing ChainArgs itself shifts ptxas' schedule of the register-capped
+// general kernels (c2 forward sweep +2%, measured).
+struct ChainArgsSc : ChainArgs {
   const double* Tbd;     // Tbd_j = Tb_j Dinv_j  (block s at ptr + s*MP*MP)
   const double* alpha;   // a_g per factor slot
 };
@@ -452,7 +457,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_fwd_kernel(ChainArg
 // per row two segments stream through the register ring (Dinv_j, Tbd_j against the same u_j);
 // the epilogue stores y_j and forms u_{j+1} from the prefetched F tile.
 template <int MP, int KT, int WR, int WC, int NF_ = -1, int NY_ = -1, int PF_ = -1, int MINB_ = 1, int FULL_ = 0>
-__global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_fwd_sc_kernel(ChainArgs a) {
+__global__ void __launch_bounds__(32 * WR * WC, MINB_) chain_fwd_sc_kernel(ChainArgsSc a) {
   using Cfg = ChainCfg<MP, KT, WR, WC, 2, NY_, PF_>;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, LD = Cfg::LD, NT = Cfg::NT, PF = Cfg::PF, GPS = Cfg::GPS;
   constexpr int NF = 2;  // F tiles of rows j+1 (read in row j's epilogue) and j+2 (in flight)
