@@ -61,6 +61,8 @@ def test_scalar_coupled_forward_matches_oracle(n, m, k, ranks):
     ref = coracle.CPlan(d, lo, up, ranks).solve(f)
     assert np.abs(x - ref).max() <= 1e-9 * np.abs(ref).max()
     assert _residual(d, lo, up, x, f) <= 1e-10
+    for _ in range(2):  # host pipeline: graph capture, replay
+        assert np.array_equal(plan_solve(plan, f), x)
     # device-resident and in-place solves take the same kernels
     ft = torch.from_numpy(f).cuda()
     xt = plan_solve(plan, ft)
