@@ -455,6 +455,7 @@ struct btd_plan {
   struct Scratch {
     int64_t k = 0;
     DevBuf ft, zbuf, xt, partial, tpartial, fcopy;
+    DevBuf ubuf;  // mode 1, scalar-coupled plan: u_j = f_g + a_g y_{j-1} of the live ranges, one row step
     cudaStream_t own = nullptr;  // graph replay stream
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     cudaStream_t side = nullptr;  // mode 1: base-accumulation GEMMs beside the row steps
@@ -981,7 +982,8 @@ void build_local(btd_plan& pl, const double* diag, const double* lower, const do
       sc_on = e ? atoi(e) : 1;
     }
     pl.scoup = 0;
-    if (sc_on && pl.mode == 0 && m == mp && mp >= 64 && cap > 0 && nrl > 0) {
+    // chain kernels (mode 0, orders 64 / 128 / 256) and the GEMM-per-row sweep (mode 1)
+    if (sc_on && m == mp && cap > 0 && nrl > 0 && ((pl.mode == 0 && mp >= 64) || pl.mode == 1)) {
       DevBuf bad;
       bad.alloc(sizeof(int));
       sc_alpha.alloc((size_t)nrl * cap * sizeof(double));
@@ -1019,8 +1021,9 @@ void build_local(btd_plan& pl, const double* diag, const double* lower, const do
   pl.off_Z = take(1);
   pl.off_I = take(1);
   if (pl.scoup) {
-    // Tbd takes over the AD section once the build no longer needs AD (a scalar-coupled plan never
-    // runs the general forward sweep: launch_chain_slice covers every shape with chain_fwd_sc_kernel)
+    // mode 0: Tbd takes over the AD section once the build no longer needs AD (a scalar-coupled plan
+    // never runs the general forward sweep: launch_chain_slice covers every shape with
+    // chain_fwd_sc_kernel).  Mode 1 keeps Tb (its base accumulation is a GEMM of its own on y_j).
     pl.off_Tbd = pl.off_AD;
     pl.off_al = take((nslot + blk - 1) / blk);  // a_g per slot, as doubles inside the pool (plan images carry it)
   }
@@ -1107,8 +1110,9 @@ void build_local(btd_plan& pl, const double* diag, const double* lower, const do
                       mp)},
                 st);
     if (pl.scoup) {  // Tbd_s = Tb_s Dinv_s for every slot, over AD (G_j = AD_j G_{j-1} is done); a_g beside it
-      launch_gemm(mp, mp, (int)nslot, mk(pool, nullptr, pl.off_Tbd, blk, mp), none(), 0.0,
-                  {term(mk(pool, nullptr, pl.off_Tb, blk, mp), mk(pool, nullptr, pl.off_Dinv, blk, mp), mp)}, st);
+      if (pl.mode == 0)
+        launch_gemm(mp, mp, (int)nslot, mk(pool, nullptr, pl.off_Tbd, blk, mp), none(), 0.0,
+                    {term(mk(pool, nullptr, pl.off_Tb, blk, mp), mk(pool, nullptr, pl.off_Dinv, blk, mp), mp)}, st);
       CK(cudaMemcpyAsync(pool + pl.off_al * blk, sc_alpha.p, (size_t)nslot * sizeof(double), cudaMemcpyDeviceToDevice,
                          st));
     }
@@ -1691,6 +1695,7 @@ void ensure_scratch(btd_plan& pl, int64_t K) {
       }
   }
   if (pbytes) S.partial.alloc(pbytes);
+  if (pl.mode == 1 && pl.scoup) S.ubuf.alloc((size_t)std::max<int64_t>(pl.nrl, 1) * pl.m * K * sizeof(double));
   S.k = K;
 }
 
@@ -1709,6 +1714,22 @@ ChainArgs chain_args(btd_plan& pl, const double* F, double* X, int64_t K, double
   a.xt = pl.S().xt.d() + pl.q0 * pl.mp * K;
   return a;
 }
+
+}  // namespace
+namespace btd {
+// Mode 1, scalar-coupled plan: u_b = F[lo_b + 1 + j] + a_{slot0_b + j} X[lo_b + j] for the live ranges b
+__global__ void sc_axpy_kernel(double* U, const double* F, const double* X, const int64_t* lo, const int64_t* slot0,
+                               const double* alpha, int64_t j, int64_t mK) {
+  const int b = blockIdx.y;
+  const double a = alpha[slot0[b] + j];
+  const double* f = F + (lo[b] + 1 + j) * mK;
+  const double* y = X + (lo[b] + j) * mK;
+  double* u = U + (int64_t)b * mK;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < mK; e += (int64_t)gridDim.x * blockDim.x)
+    u[e] = fma(a, y[e], f[e]);
+}
+}  // namespace btd
+namespace {
 
 // Forward sweeps of the owned ranges: y rows into X, base_q into base (+ q*base_stride)
 void solve_forward(btd_plan& pl, const double* F, double* X, int64_t K, double* base, int64_t base_stride,
@@ -1748,10 +1769,17 @@ void solve_forward(btd_plan& pl, const double* F, double* X, int64_t K, double* 
     const auto& s = pl.steps1[j];
     if (s.cnt == 0) break;
     const SplitK* ssp = step_split(pl, s.cnt, K);  // few ranges (sharded): split the reductions
-    if (j == 0)
+    if (j == 0) {
       launch_gemm(m, K, s.cnt, mk(X, pl.d_lo, 1, mK, K), none(), 0.0,
                   {term(mk(pool, pl.d_slot0, pl.off_Dinv, blk, mp), mk(F, pl.d_lo, 1, mK, K), m)}, st, ssp);
-    else
+    } else if (pl.scoup) {  // y_j = Dinv_j (f_g + a_g y_{j-1}): one product per row step instead of two
+      double* U = S.ubuf.d();
+      dim3 grid((unsigned)std::min<int64_t>((mK + 255) / 256, 296), (unsigned)s.cnt);
+      btd::sc_axpy_kernel<<<grid, 256, 0, st>>>(U, F, X, pl.d_lo, pl.d_slot0, pool + pl.off_al * blk, j, mK);
+      CK_LAUNCH();
+      launch_gemm(m, K, s.cnt, mk(X, pl.d_lo, 1 + j, mK, K), none(), 0.0,
+                  {term(mk(pool, pl.d_slot0, pl.off_Dinv + j, blk, mp), mk(U, nullptr, 0, mK, K), m)}, st, ssp);
+    } else
       launch_gemm(m, K, s.cnt, mk(X, pl.d_lo, 1 + j, mK, K), none(), 0.0,
                   {term(mk(pool, pl.d_slot0, pl.off_Dinv + j, blk, mp), mk(F, pl.d_lo, 1 + j, mK, K), m),
                    term(mk(pool, pl.d_slot0, pl.off_AD + j, blk, mp), mk(X, pl.d_lo, j, mK, K), m)},

@@ -43,6 +43,7 @@ CASES = [
     (96, 64, 128, 4), (96, 64, 37, 4), (200, 64, 256, 37),
     (60, 128, 64, 5), (60, 128, 19, 5),
     (48, 256, 16, 4), (48, 256, 21, 4), (80, 256, 64, 37),
+    (24, 320, 16, 3), (20, 512, 33, 4),   # block orders above 256: the GEMM-per-row sweep (mode 1)
 ]
 
 
@@ -106,6 +107,25 @@ def test_detection_is_exact():
     assert not plan.scalar_coupling
     ref = coracle.CPlan(d4, lo4, up4, 3).solve(f4)
     assert np.abs(plan_solve(plan, f4) - ref).max() <= 1e-9 * np.abs(ref).max()
+
+
+def test_forced_gemm_sweep_small_blocks(monkeypatch):
+    """BTD_FORCE_MODE=1 on a 64-block plan: the mode-1 form u_j = f + a y_{j-1}, y_j = Dinv_j u_j."""
+    import coracle
+    import torch
+
+    from paper_1108_4181_b200 import BlockTriMatrix, plan_build, plan_solve
+
+    torch.cuda.set_device(0)
+    monkeypatch.setenv("BTD_FORCE_MODE", "1")
+    d, lo, up, f = _scalar_lower(50, 64, 24, seed=31)
+    plan = plan_build(BlockTriMatrix(d, lo, up), 5)
+    assert plan.mode == 1 and plan.scalar_coupling
+    x = plan_solve(plan, f)
+    ref = coracle.CPlan(d, lo, up, 5).solve(f)
+    assert np.abs(x - ref).max() <= 1e-9 * np.abs(ref).max()
+    ft = torch.from_numpy(f).cuda()
+    assert np.array_equal(plan_solve(plan, ft).cpu().numpy(), x)
 
 
 def test_config1_family_is_scalar_coupled():
